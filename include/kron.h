@@ -1,0 +1,140 @@
+/* include/kron.h — C-ABI of libkron, the B200 (sm_100a) Kron-Matmul library.
+ *
+ * Operation ("Kron-Matmul"):
+ *     Y[M x prod_i Q_i] = X[M x prod_i P_i] . (F^1 (x) F^2 (x) ... (x) F^N)
+ * computed as one sliced multiply per factor, F^N first (Algorithm 1):
+ *     T'[m, q*(W/P) + s] = sum_p T[m, s*P + p] * F[p, q]           (W = width of T)
+ * with consecutive factors fused in shared memory and results stored directly at
+ * their next-iteration positions, so no transpose ever runs.
+ *
+ * Conventions shared by every entry point
+ *   Layout     all matrices dense, row-major, leading dimension = column count, same dtype.
+ *   Factors    P[i], Q[i] (host arrays, length N) give F[i] = F^{i+1} as a P[i] x Q[i] matrix;
+ *              F[0] = F^1 is the MOST significant factor of the Kronecker product.
+ *              F is a host array of N device pointers.
+ *   Pointers   X, F[i], Y, workspace, X_local, Y_local are DEVICE pointers on the current device.
+ *   Ownership  the caller owns X, F and Y.  X and F are read-only; Y is write-only and must not
+ *              overlap X or any F[i].  kron_matmul() allocates its workspace stream-ordered
+ *              (cudaMallocAsync on `stream`) and frees it stream-ordered; kron_matmul_ws() uses
+ *              caller memory instead.
+ *   Streams    `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  All
+ *              work is enqueued on it; the call returns without synchronising.
+ *   Errors     argument / shape problems are reported synchronously, BEFORE any work is
+ *              enqueued.  Kernel faults are asynchronous (CUDA semantics) and surface at the
+ *              next synchronising call.  The library never aborts and never prints.
+ *   M = 0      a successful no-op.
+ *   Threads    reentrant and thread-safe across distinct streams (the plan cache is locked).
+ */
+#ifndef KRON_H_
+#define KRON_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { KRON_F32 = 0, KRON_F64 = 1 } kron_dtype_t;
+
+typedef enum {
+  KRON_OK = 0,
+  KRON_ERR_INVALID_ARG = 1, /* null pointer, N < 1, P_i < 1, Q_i < 1, bad dtype, M < 0, bad grid  */
+  KRON_ERR_SHAPE = 2,       /* prod P or prod Q overflows int64 / exceeds addressable memory, or  */
+                            /* a caller buffer (workspace) is too small                           */
+  KRON_ERR_UNSUPPORTED = 3, /* no kernel for this configuration (not returned for valid shapes)   */
+  KRON_ERR_NO_MEMORY = 4,   /* workspace allocation failed                                        */
+  KRON_ERR_CUDA = 5,        /* a CUDA launch / API call failed                                    */
+  KRON_ERR_NCCL = 6,        /* NCCL unavailable or an NCCL call failed (distributed path)         */
+  KRON_ERR_DIST_LAYOUT = 7  /* distributed shape does not partition: GM !| M, GK !| K or L, or no */
+                            /* legal round plan exists                                            */
+} kron_status_t;
+
+/* Human-readable name of a status code (static storage; never NULL). */
+const char *kron_status_string(kron_status_t s);
+
+/* ---------------------------------------------------------------------------------------------
+ * Single GPU — Algorithm 1 + fusion.
+ *
+ * kron_matmul: Y = X . (F^1 (x) ... (x) F^N).  M >= 0, N >= 1, P[i], Q[i] >= 1.
+ * The library plans the factor passes (cached per (device, M, shapes, dtype)), reserves its
+ * workspace stream-ordered on `stream`, and enqueues one kernel per pass.                      */
+kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                          const void *const *F, void *Y, kron_dtype_t dtype, void *stream);
+
+/* Bytes of workspace kron_matmul_ws() needs for this problem (0 when none). */
+kron_status_t kron_matmul_workspace_size(int64_t M, int32_t N, const int32_t *P, const int32_t *Q,
+                                         kron_dtype_t dtype, size_t *bytes);
+
+/* kron_matmul with a caller-owned device workspace of `workspace_bytes` bytes (>= the size
+ * above; KRON_ERR_SHAPE otherwise).  The workspace must not overlap X, F or Y.               */
+kron_status_t kron_matmul_ws(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                             const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                             size_t workspace_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------------------------
+ * Planner introspection (host only; no GPU needed).  Describes the pass plan kron_matmul uses:
+ * pass i applies factors F^{first[i]}, F^{first[i]-1}, ..., F^{first[i]-nfactors[i]+1}
+ * (1-based, processing order N -> 1) with kernel family kind[i] (0 generic, 1 fused small-P,
+ * 2 GEMM-style large-P).  Arrays have room for `cap` passes; *npasses receives the count.     */
+kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const int32_t *Q,
+                                 kron_dtype_t dtype, int32_t cap, int32_t *npasses, int32_t *first,
+                                 int32_t *nfactors, int32_t *kind);
+
+/* Algorithmic HBM bytes and FLOPs of the plan:
+ *   bytes = sum_passes s*M*(W_in + W_out) + sum_f s*P_f*Q_f,   flops = sum_f 2*M*W_f*Q_f.      */
+kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                             double *hbm_bytes, double *flops);
+
+/* ---------------------------------------------------------------------------------------------
+ * Distributed — Algorithm 2 on a {GM, GK} grid of ranks (one process per GPU).
+ *
+ * Rank r has grid coordinates {gM, gK} = {r / GK, r % GK}.  It holds
+ *     X_local = X[gM*M/GM : +M/GM][gK*K/GK : +K/GK]          (M/GM x K/GK, row-major)
+ * and receives
+ *     Y_local = Y[gM*M/GM : +M/GM][gK*L/GK : +L/GK]          (M/GM x L/GK, row-major).
+ * Factors are replicated on every rank.  Each round performs as many sliced multiplies
+ * as the local column block allows and then ONE all-to-all among the GK ranks of
+ * the row group regroups the slices (lines 676-692; reading G13).
+ *
+ * Context creation.  `backend` selects the exchange:
+ *     0  NCCL: `nccl_unique_id` points to the 128-byte ncclUniqueId created by rank 0 and
+ *        broadcast by the caller (e.g. over a torch ProcessGroup); world_size = GM*GK ranks,
+ *        one per GPU; `rank` is this process's rank.  The row-group communicator is
+ *        ncclCommSplit(world, color = gM, key = gK).
+ *     1  virtual: ONE process drives all GM*GK ranks on the current device; the exchange is a
+ *        device-to-device copy (used to test the distributed data path on a single GPU).
+ *        nccl_unique_id and rank are ignored.
+ * GM = GK = 0 selects the grid by the paper's rule.                               */
+typedef struct kron_dist_ctx kron_dist_ctx_t;
+
+kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, int32_t world_size,
+                                   int32_t rank, int32_t GM, int32_t GK, kron_dist_ctx_t **out);
+kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx);
+/* Grid actually used by the context. */
+kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_t *GK);
+/* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
+kron_status_t kron_dist_nccl_unique_id(void *out128);
+
+/* Collective over the context's ranks: every rank calls it with identical M, N, P, Q, dtype.
+ * NCCL backend: X_local / Y_local are this rank's blocks.
+ * Virtual backend: X_local / Y_local are host arrays of GM*GK device pointers, one per rank.
+ * Errors: GM !| M, GK !| K, GK !| L or no legal round plan -> KRON_ERR_DIST_LAYOUT (shape-only,
+ * so every rank returns the same status).  NCCL failures -> KRON_ERR_NCCL.                    */
+kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X_local,
+                               const void *const *F, void *Y_local, kron_dtype_t dtype, kron_dist_ctx_t *ctx,
+                               void *stream);
+
+/* Round plan of the distributed path (host only).  On return rounds[j] = number of factors the
+ * j-th round applies locally (sum = N), *nrounds the count; ledger[j] (optional) = values sent
+ * between distinct ranks in round j summed over all ranks = M * W_j * (GK-1)/GK (reading G12). */
+kron_status_t kron_dist_plan(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, int32_t GM, int32_t GK,
+                             int32_t cap, int32_t *nrounds, int32_t *rounds, int64_t *ledger);
+
+/* Grid rule of P:654-655 ({sqrt G, sqrt G}, else {2^ceil(log2 sqrt G), 2^floor(log2 sqrt G)}). */
+kron_status_t kron_dist_grid_rule(int32_t G, int32_t *GM, int32_t *GK);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KRON_H_ */

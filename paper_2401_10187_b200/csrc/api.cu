@@ -1,0 +1,334 @@
+// api.cu — the libkron C-ABI (include/kron.h): validation, the pass planner (Algorithm 1 loop +
+// fusion groups), the plan cache, workspace handling and dispatch.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kron_internal.h"
+
+namespace kron {
+
+namespace {
+
+int es_of(int dtype) { return dtype == KRON_F32 ? 4 : 8; }
+
+bool mul_ok(int64_t a, int64_t b, int64_t lim, int64_t *out) {
+  if (a != 0 && b > lim / a) return false;
+  *out = a * b;
+  return true;
+}
+
+// Tile geometry of a fused group: C = P^k chunk, R chunks per tile row
+// (output runs of R*s >= 32 bytes), tileK = R*C columns, tileM rows; all TMA box constraints.
+bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, PassPlan *pp) {
+  const int es = es_of(inst.dtype), line = 128 / es;
+  const int p = inst.P;
+  int64_t C = 1;
+  for (int i = 0; i < k; ++i) C *= p;
+  const int64_t E = inst.elems();
+  if (W % line || W % C || C > E) return false;
+  const int64_t WC = W / C;
+  if ((WC * es) % 16) return false;
+  int64_t R = E / C;
+  if (R > WC) R = WC;
+  if (R > 256) R = 256;
+  if (R * es < 32 || (R * es) % 16) return false;
+  const int64_t tileK = R * C;
+  if (tileK % line) return false;
+  const int64_t lines = tileK / line;
+  if (lines > 256 && lines % 256) return false;
+  int64_t tileM = E / tileK;
+  if (tileM > M) tileM = M;
+  if (tileM > 256) tileM = 256;
+  if (tileM < 1) tileM = 1;
+  if (tileM > 1 && lines > 256) return false;
+  if (C > 256 && (C % 256 || C / 256 > 256)) return false;
+  const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
+  const int stages = stage <= 32 * 1024 ? 3 : 2;
+  const int64_t smem = 1024 + stages * stage + (int64_t)k * p * p * es + 16 + 8 * stages;
+  if (smem > 227 * 1024) return false;
+  pp->kind = KIND_FUSED;
+  pp->nf = k;
+  pp->P = pp->Q = p;
+  pp->C = C;
+  pp->Qc = C;
+  pp->R = (int)R;
+  pp->tileK = tileK;
+  pp->tileM = (int)tileM;
+  pp->stages = stages;
+  return true;
+}
+
+struct PlanKey {
+  int dev;
+  int64_t M;
+  int dtype;
+  std::vector<int32_t> P, Q;
+  bool operator<(const PlanKey &o) const {
+    if (dev != o.dev) return dev < o.dev;
+    if (M != o.M) return M < o.M;
+    if (dtype != o.dtype) return dtype < o.dtype;
+    if (P != o.P) return P < o.P;
+    return Q < o.Q;
+  }
+};
+
+std::mutex g_cache_mu;
+std::map<PlanKey, std::shared_ptr<const Plan>> g_cache;
+
+kron_status_t cached_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype,
+                          std::shared_ptr<const Plan> *out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  PlanKey key{dev, M, dtype, std::vector<int32_t>(P, P + N), std::vector<int32_t>(Q, Q + N)};
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) {
+    *out = it->second;
+    return KRON_OK;
+  }
+  auto plan = std::make_shared<Plan>();
+  kron_status_t st = make_plan(M, N, P, Q, dtype, plan.get());
+  if (st != KRON_OK) return st;
+  g_cache.emplace(key, plan);
+  *out = plan;
+  return KRON_OK;
+}
+
+kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream) {
+  const size_t es = es_of(plan.dtype);
+  void *bufs[4] = {const_cast<void *>(X), Y, ws,
+                   ws ? static_cast<char *>(ws) + (size_t)plan.ws_elems * es : nullptr};
+  for (const PassPlan &pp : plan.passes) {
+    const void *in = bufs[pp.src];
+    void *out = bufs[pp.dst];
+    int err = 0;
+    if (pp.kind == KIND_FUSED) {
+      if (!tmap_available()) return KRON_ERR_CUDA;
+      const void *grp[kMaxFused];
+      for (int i = 0; i < pp.nf; ++i) grp[i] = F[pp.first - 1 - i];
+      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, stream);
+    } else if (pp.kind == KIND_GEMM) {
+      err = launch_gemm(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
+    } else {
+      err = launch_generic(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
+    }
+    if (err != 0) return KRON_ERR_CUDA;
+  }
+  return KRON_OK;
+}
+
+size_t ws_bytes_of(const Plan &plan) {
+  return (size_t)plan.nws * (size_t)plan.ws_elems * (size_t)es_of(plan.dtype);
+}
+
+}  // namespace
+
+kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
+  if (M < 0 || N < 1 || N > kMaxFactors || !P || !Q) return KRON_ERR_INVALID_ARG;
+  if (dtype != KRON_F32 && dtype != KRON_F64) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (P[i] < 1 || Q[i] < 1) return KRON_ERR_INVALID_ARG;
+  const int64_t lim = (int64_t)1 << 50;  // elements per row; beyond any HBM
+  int64_t K = 1, L = 1;
+  for (int i = 0; i < N; ++i) {
+    if (!mul_ok(K, P[i], lim, &K) || !mul_ok(L, Q[i], lim, &L)) return KRON_ERR_SHAPE;
+  }
+  // every intermediate must fit the address space: M * width * s < 2^60
+  int64_t W = K, maxw = K;
+  for (int f = N; f >= 1; --f) {
+    W = W / P[f - 1];
+    if (!mul_ok(W, Q[f - 1], lim, &W)) return KRON_ERR_SHAPE;
+    if (W > maxw) maxw = W;
+  }
+  int64_t tot;
+  if (!mul_ok(maxw, M > 0 ? M : 1, (int64_t)1 << 57, &tot)) return KRON_ERR_SHAPE;
+  return KRON_OK;
+}
+
+kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan) {
+  kron_status_t st = validate(M, N, P, Q, dtype);
+  if (st != KRON_OK) return st;
+  plan->N = N;
+  plan->M = M;
+  plan->dtype = dtype;
+  plan->W.assign(N + 1, 0);
+  int64_t K = 1;
+  for (int i = 0; i < N; ++i) K *= P[i];
+  plan->W[N] = K;  // Alg 1
+  for (int f = N; f >= 1; --f) plan->W[f - 1] = plan->W[f] / P[f - 1] * Q[f - 1];  // line 307 / 319
+  plan->passes.clear();
+
+  const int64_t Mp = M > 0 ? M : 1;
+  int f = N;  // next factor to apply (processing order N -> 1, Alg 1)
+  while (f >= 1) {
+    const int p = P[f - 1], q = Q[f - 1];
+    const int64_t W = plan->W[f];
+    const int inst = (p == q) ? fused_find(dtype, p) : -1;
+    if (inst >= 0) {
+      int run = 1;  // consecutive factors of the same square shape
+      while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
+      int kmax = 0;
+      PassPlan probe;
+      for (int k = 1; k <= run && k <= kMaxFused; ++k)
+        if (fused_geometry(fused_instance(inst), k, W, Mp, &probe)) kmax = k;
+      if (kmax >= 1) {
+        // fewest passes, then balanced group sizes ("ceil(N/Fused) iterations")
+        const int npass = (run + kmax - 1) / kmax;
+        const int base = run / npass, extra = run % npass;
+        for (int i = 0; i < npass; ++i) {
+          const int k = base + (i < extra ? 1 : 0);
+          PassPlan pp;
+          fused_geometry(fused_instance(inst), k, W, Mp, &pp);
+          pp.variant = inst;
+          pp.first = f;
+          pp.W_in = W;
+          pp.W_out = W;  // square factors keep the width
+          plan->passes.push_back(pp);
+          f -= k;
+        }
+        continue;
+      }
+    }
+    PassPlan pp;
+    pp.first = f;
+    pp.nf = 1;
+    pp.P = p;
+    pp.Q = q;
+    pp.C = p;
+    pp.Qc = q;
+    pp.W_in = W;
+    pp.W_out = plan->W[f - 1];
+    pp.kind = gemm_supported(dtype, Mp, W, p, q) ? KIND_GEMM : KIND_GENERIC;
+    plan->passes.push_back(pp);
+    f -= 1;
+  }
+
+  // buffers (Alg 1, 318): the last pass writes Y, X is never written; interior
+  // intermediates ping-pong between the workspace and Y when Y is wide enough, else two workspaces.
+  const int np = (int)plan->passes.size();
+  int64_t max_interior = 0;
+  for (int i = 0; i + 1 < np; ++i)
+    if (plan->passes[i].W_out > max_interior) max_interior = plan->passes[i].W_out;
+  const bool y_alt = max_interior <= plan->W[0];
+  plan->nws = np <= 1 ? 0 : (y_alt || np == 2 ? 1 : 2);
+  plan->ws_elems = np <= 1 ? 0 : M * max_interior;
+  for (int i = np - 1, k = 0; i >= 0; --i, ++k) {
+    int dst;
+    if (k == 0) dst = BUF_Y;
+    else if (y_alt) dst = (k % 2 == 1) ? BUF_WS0 : BUF_Y;
+    else dst = (k % 2 == 1) ? BUF_WS0 : BUF_WS1;
+    plan->passes[i].dst = dst;
+  }
+  for (int i = 0; i < np; ++i) plan->passes[i].src = i == 0 ? BUF_X : plan->passes[i - 1].dst;
+  return KRON_OK;
+}
+
+}  // namespace kron
+
+using namespace kron;
+
+extern "C" {
+
+const char *kron_status_string(kron_status_t s) {
+  switch (s) {
+    case KRON_OK: return "KRON_OK";
+    case KRON_ERR_INVALID_ARG: return "KRON_ERR_INVALID_ARG";
+    case KRON_ERR_SHAPE: return "KRON_ERR_SHAPE";
+    case KRON_ERR_UNSUPPORTED: return "KRON_ERR_UNSUPPORTED";
+    case KRON_ERR_NO_MEMORY: return "KRON_ERR_NO_MEMORY";
+    case KRON_ERR_CUDA: return "KRON_ERR_CUDA";
+    case KRON_ERR_NCCL: return "KRON_ERR_NCCL";
+    case KRON_ERR_DIST_LAYOUT: return "KRON_ERR_DIST_LAYOUT";
+  }
+  return "KRON_ERR_UNKNOWN";
+}
+
+kron_status_t kron_matmul_workspace_size(int64_t M, int32_t N, const int32_t *P, const int32_t *Q,
+                                         kron_dtype_t dtype, size_t *bytes) {
+  if (!bytes) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> plan;
+  kron_status_t st = cached_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  *bytes = M == 0 ? 0 : ws_bytes_of(*plan);
+  return KRON_OK;
+}
+
+kron_status_t kron_matmul_ws(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                             const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                             size_t workspace_bytes, void *stream) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X || !F || !Y) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> plan;
+  st = cached_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  const size_t need = ws_bytes_of(*plan);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return KRON_ERR_SHAPE;
+  return run_plan(*plan, X, F, Y, workspace, stream);
+}
+
+kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                          const void *const *F, void *Y, kron_dtype_t dtype, void *stream) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X || !F || !Y) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> plan;
+  st = cached_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  const size_t need = ws_bytes_of(*plan);
+  void *ws = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (need > 0) {
+    if (cudaMallocAsync(&ws, need, s) != cudaSuccess) {
+      cudaGetLastError();
+      return KRON_ERR_NO_MEMORY;
+    }
+  }
+  st = run_plan(*plan, X, F, Y, ws, stream);
+  if (ws) cudaFreeAsync(ws, s);
+  return st;
+}
+
+kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                 int32_t cap, int32_t *npasses, int32_t *first, int32_t *nfactors, int32_t *kind) {
+  if (!npasses) return KRON_ERR_INVALID_ARG;
+  Plan plan;
+  kron_status_t st = make_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  *npasses = (int32_t)plan.passes.size();
+  for (int i = 0; i < (int)plan.passes.size() && i < cap; ++i) {
+    if (first) first[i] = plan.passes[i].first;
+    if (nfactors) nfactors[i] = plan.passes[i].nf;
+    if (kind) kind[i] = plan.passes[i].kind;
+  }
+  return KRON_OK;
+}
+
+kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                             double *hbm_bytes, double *flops) {
+  Plan plan;
+  kron_status_t st = make_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  const double es = es_of((int)dtype);
+  double b = 0, fl = 0;
+  for (const PassPlan &pp : plan.passes) b += es * (double)M * (double)(pp.W_in + pp.W_out);
+  for (int i = 0; i < N; ++i) b += es * (double)P[i] * Q[i];
+  for (int f = 1; f <= N; ++f) fl += 2.0 * (double)M * (double)plan.W[f] * Q[f - 1];
+  if (hbm_bytes) *hbm_bytes = b;
+  if (flops) *flops = fl;
+  return KRON_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,70 @@
+// kron_internal.h — host-side plan structures and kernel launchers shared by the libkron sources.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include "../../include/kron.h"
+
+namespace kron {
+
+enum Kind { KIND_GENERIC = 0, KIND_FUSED = 1, KIND_GEMM = 2 };
+enum Buf { BUF_X = 0, BUF_Y = 1, BUF_WS0 = 2, BUF_WS1 = 3 };
+
+constexpr int kMaxFactors = 64;
+constexpr int kMaxFused = 8;
+
+// One kernel launch: applies factors F^{first}, F^{first-1}, ..., F^{first-nf+1} (1-based).
+struct PassPlan {
+  int kind = KIND_GENERIC;
+  int first = 0;  // 1-based index of the first factor this pass applies (processing order N -> 1)
+  int nf = 1;     // factors fused in this pass
+  int P = 0, Q = 0;           // factor shape (uniform within a fused group; P == Q for KIND_FUSED)
+  int64_t W_in = 0, W_out = 0;  // row widths entering / leaving the pass
+  int64_t C = 1, Qc = 1;      // chunk = prod P over the group, composite columns = prod Q
+  // fused-kernel tiling: a tile is tileM rows x tileK = R*C columns
+  int R = 0, tileM = 1;
+  int64_t tileK = 0;
+  int variant = -1;  // fused: kernel instance id; gemm: instance id
+  int stages = 2;
+  int src = BUF_X, dst = BUF_Y;
+};
+
+struct Plan {
+  int N = 0;
+  int64_t M = 0;
+  int dtype = 0;
+  std::vector<int64_t> W;  // W[f], f = 0..N (W[N] = K, W[0] = L)
+  std::vector<PassPlan> passes;
+  int nws = 0;             // workspace buffers (0, 1 or 2)
+  int64_t ws_elems = 0;    // elements per workspace buffer
+};
+
+// Builds the plan (host only).  Returns KRON_OK or a validation error.
+kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out);
+kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype);
+
+// ---- fused small-P kernel family (fused.cu)
+struct FusedInstance {
+  int dtype;  // 0 f32, 1 f64
+  int P;
+  int NT;     // threads per CTA
+  int RS;     // slices per thread
+  int64_t elems() const { return (int64_t)NT * RS * P; }
+};
+int fused_instance_count();
+const FusedInstance &fused_instance(int i);
+int fused_find(int dtype, int P);  // instance id or -1
+
+// ---- launchers (device code lives in the .cu files).  Return cudaError_t as int.
+int launch_generic(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F,
+                   void *stream);
+int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
+                 void *stream);
+int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
+bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
+
+// tensor-map encoder (driver entry point fetched through the runtime)
+bool tmap_available();
+
+}  // namespace kron

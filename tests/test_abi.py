@@ -1,0 +1,141 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/kron.h declares, rejects bad
+arguments synchronously, and its host-side planner (pass plan, costs, distributed round plan) obeys
+the paper's rules.  No compute calls (no GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def kron():
+    from paper_2401_10187_b200 import build
+    build.build()
+    from paper_2401_10187_b200 import kron as k
+    return k
+
+
+def header_symbols():
+    with open(os.path.join(ROOT, "include", "kron.h")) as f:
+        text = f.read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(kron_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_exports_every_declared_symbol(kron):
+    syms = header_symbols()
+    assert "kron_matmul" in syms and "kron_matmul_dist" in syms and len(syms) >= 12
+    lib = ctypes.CDLL(kron.lib_path)
+    for s in syms:
+        assert hasattr(lib, s), f"libkron.so does not export {s}"
+
+
+def test_status_strings(kron):
+    lib = kron.raw_lib()
+    for code, name in kron.STATUS.items():
+        assert lib.kron_status_string(code).decode() == name
+
+
+def _call(kron, M, P, Q, dtype=0, X=1, F=True, Y=1):
+    lib = kron.raw_lib()
+    n = len(P)
+    Pa = (ctypes.c_int32 * max(n, 1))(*P) if n else None
+    Qa = (ctypes.c_int32 * max(n, 1))(*Q) if n else None
+    Fp = (ctypes.c_void_p * max(n, 1))(*([1] * n)) if F else None
+    return lib.kron_matmul(M, n, Pa, Qa, X, Fp, Y, dtype, None)
+
+
+def test_argument_errors_are_synchronous(kron):
+    assert _call(kron, 4, [2, 2], [2, 2], X=None) == 1      # null X
+    assert _call(kron, 4, [2, 2], [2, 2], F=False) == 1     # null F
+    assert _call(kron, 4, [], []) == 1                      # N < 1
+    assert _call(kron, 4, [2, 0], [2, 2]) == 1              # P_i < 1
+    assert _call(kron, 4, [2, 2], [2, -1]) == 1             # Q_i < 1
+    assert _call(kron, 4, [2, 2], [2, 2], dtype=7) == 1     # bad dtype
+    assert _call(kron, -1, [2, 2], [2, 2]) == 1             # M < 0
+    assert _call(kron, 4, [2 ** 30] * 3, [2] * 3) == 2      # prod P overflows
+    assert _call(kron, 0, [2, 2], [2, 2], X=None, Y=None) == 0  # M = 0: no-op
+
+
+def test_plan_configs(kron):
+    f32, f64 = "float32", "float64"
+    # config B: 6 x (8x8) fp32 -> two fused passes of 3 (Fused = 3 at B200 capacity)
+    assert kron.plan_describe(1024, [8] * 6, [8] * 6, f32) == [(6, 3, "fused"), (3, 3, "fused")]
+    # config C: 4 x (32x32) -> (2,2) in fp32 and fp64
+    assert kron.plan_describe(1024, [32] * 4, [32] * 4, f32) == [(4, 2, "fused"), (2, 2, "fused")]
+    assert kron.plan_describe(1024, [32] * 4, [32] * 4, f64) == [(4, 2, "fused"), (2, 2, "fused")]
+    # config A: K = 16 is narrower than one 128-byte TMA line -> generic
+    assert [k for _, _, k in kron.plan_describe(16, [4, 4], [4, 4], f32)] == ["generic", "generic"]
+    # every plan applies every factor exactly once, N -> 1
+    for P, Q, dt in [([16] * 5, [16] * 5, f32), ([128] * 3, [128] * 3, f64), ([64] * 3, [32] * 3, f64),
+                     ([3, 8, 8, 8, 5], [4, 8, 8, 8, 2], f32), ([2] * 12, [2] * 12, f64)]:
+        plan = kron.plan_describe(64, P, Q, dt)
+        covered = []
+        for first, nf, _ in plan:
+            covered += list(range(first, first - nf, -1))
+        assert covered == list(range(len(P), 0, -1))
+
+
+def test_plan_cost_closed_forms(kron):
+    # FLOPs = sum_f 2 M W_f Q_f (north_star); for square factors = 2 N M P K
+    b, fl = kron.plan_cost(1024, [8] * 6, [8] * 6, "float32")
+    assert fl == 2 * 6 * 1024 * 8 * 8 ** 6
+    # bytes of the (3,3) plan: two passes, each reads and writes M*K fp32, plus the factors
+    assert b == 2 * 2 * 4 * 1024 * 8 ** 6 + 6 * 4 * 64
+    W = oracle.widths([64] * 3, [32] * 3)
+    _, fl2 = kron.plan_cost(320, [64] * 3, [32] * 3, "float64")
+    assert fl2 == sum(2 * 320 * W[f] * 32 for f in range(1, 4))
+
+
+def test_workspace_sizes(kron):
+    # one pass: no workspace; P = Q: Y doubles as the other ping-pong buffer -> one M x K buffer
+    assert kron.workspace_size(16, [4], [4], "float32") == 0
+    assert kron.workspace_size(1024, [8] * 6, [8] * 6, "float32") == 1024 * 8 ** 6 * 4
+    # mixed widths (G2): interior width 64 > L = 16 needs the workspace sized by the widest interior
+    ws = kron.workspace_size(10, [8, 2], [2, 8], "float64")
+    assert ws >= 10 * 64 * 8
+
+
+def test_grid_rule_matches_oracle(kron):
+    for G in [1, 2, 4, 8, 16, 32, 64]:
+        assert kron.grid_rule(G) == oracle.grid(G)
+    with pytest.raises(kron.KronError):
+        kron.grid_rule(6)
+
+
+@pytest.mark.parametrize("M,P,Q,GM,GK", [
+    (1, [4] * 4, [4] * 4, 1, 4),
+    (8, [16] * 5, [16] * 5, 4, 2),
+    (4, [16] * 5, [16] * 5, 2, 2),
+    (4, [4] * 5, [4] * 5, 2, 4),
+    (6, [8, 4, 4], [4, 8, 4], 2, 2),
+    (2, [2] * 6, [2] * 6, 1, 4),
+])
+def test_dist_plan_legal_and_ledger_matches_oracle(kron, M, P, Q, GM, GK):
+    rounds, ledger = kron.dist_plan(M, P, Q, GM, GK)
+    assert sum(rounds) == len(P)
+    seed = synth.SEED_BASE + 11
+    X = synth.matrix(M, int(np.prod(P)), seed, 0, "int")
+    Fs = synth.factors(P, Q, seed, "int")
+    Y, oled = oracle.alg2(X, Fs, GM, GK, rounds)  # the oracle simulator rejects illegal rounds
+    assert oled == ledger
+    assert np.array_equal(Y, oracle.alg1(X, Fs))
+
+
+def test_dist_plan_paper_local(kron):
+    # Fig 8 / Alg 2: {1,4}, K = 256, P = 4 -> Local_max = floor(log_4 64) = 3; N = 4 -> 2 rounds,
+    # ledger 2 * 256 * 3/4 = 384
+    rounds, ledger = kron.dist_plan(1, [4] * 4, [4] * 4, 1, 4)
+    assert len(rounds) == 2 and sum(ledger) == 384
+    # config E at the paper grid {4,2}: Local_max = floor(log_16 2^19) = 4, N = 5 -> 2 exchanges
+    rounds, ledger = kron.dist_plan(4096, [16] * 5, [16] * 5, 4, 2)
+    assert len(rounds) == 2 and sorted(rounds) == [2, 3]
+    with pytest.raises(kron.KronError):
+        kron.dist_plan(4095, [16] * 5, [16] * 5, 4, 2)  # GM does not divide M

@@ -1,0 +1,163 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bars: bit-exact on small-integer data (fp64 {-2..2}, fp32 {-1,0,1}: every partial
+sum is an exact integer, so any summation order gives identical bits); max relative error <= 1e-5
+(fp32) / 1e-12 (fp64) on U[0,1) data (positive: no cancellation); componentwise-normwise error on
+signed data.  Sizes span several tiles plus ragged row blocks; full BASELINE sizes are checked on
+sampled rows (the oracle computes rows independently).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {np.float32: 1e-5, np.float64: 1e-12}
+
+
+@pytest.fixture(scope="module")
+def kron(cuda_device):
+    from paper_2401_10187_b200 import kron as k
+    return k
+
+
+def to_dev(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def run(kron, X, Fs, dev):
+    import torch
+    Y = kron.matmul(to_dev(X, dev), [to_dev(f, dev) for f in Fs])
+    torch.cuda.synchronize()
+    return Y.cpu().numpy()
+
+
+def case(M, P, Q, dt, mode, seed_off=0):
+    seed = synth.SEED_BASE + 1000 + seed_off
+    X = synth.matrix(M, int(np.prod(P)), seed, 0, mode, dt)
+    Fs = synth.factors(P, Q, seed, mode, dt)
+    return X, Fs
+
+
+def rel_err(Y, ref):
+    return float(np.max(np.abs(Y.astype(np.float64) - ref) / np.abs(ref)))
+
+
+SMALL = [
+    # (M, P, Q) — covers every kernel family and the degenerate cases
+    (16, [4, 4], [4, 4]),                 # config A (generic)
+    (17, [4] * 4, [4] * 4),               # fused P=4, ragged row block (tileM rows)
+    (33, [8] * 4, [8] * 4),               # fused P=8 (3,1)
+    (5, [8] * 6, [8] * 6),                # config B shape, small M
+    (3, [16] * 4, [16] * 4),              # fused P=16 (2,2)
+    (2, [32] * 3, [32] * 3),              # fused P=32 (2,1)
+    (9, [2] * 10, [2] * 10),              # fused P=2 deep groups
+    (1, [8] * 5, [8] * 5),                # single row
+    (7, [3, 5, 2], [2, 4, 3]),            # odd non-square -> generic
+    (4, [8, 2], [2, 8]),                  # mixed widths (G2)
+    (6, [5, 8, 8, 8], [5, 8, 8, 8]),      # odd leading factor + fused 8-run
+    (3, [64, 64], [32, 32]),              # non-square large P
+    (2, [128, 16], [128, 16]),            # large P then small
+    (4, [7], [9]),                        # N = 1: plain GEMM
+    (3, [1, 4, 1], [2, 4, 1]),            # P_i or Q_i = 1
+]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("M,P,Q", SMALL)
+def test_bit_exact_integer(kron, cuda_device, M, P, Q, dt):
+    mode = "int1" if dt == np.float32 else "int"
+    X, Fs = case(M, P, Q, dt, mode)
+    ref = oracle.alg1(X, Fs)
+    assert np.max(np.abs(ref)) < (2 ** 24 if dt == np.float32 else 2 ** 53)
+    Y = run(kron, X, Fs, cuda_device)
+    assert Y.dtype == dt
+    assert np.array_equal(Y, ref.astype(dt)), f"max |diff| {np.max(np.abs(Y - ref))}"
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("M,P,Q", SMALL)
+def test_random_relative_error(kron, cuda_device, M, P, Q, dt):
+    X, Fs = case(M, P, Q, dt, "urand", 1)
+    ref = oracle.alg1(X, Fs)
+    Y = run(kron, X, Fs, cuda_device)
+    assert rel_err(Y, ref) <= TOL[dt]
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+def test_signed_componentwise(kron, cuda_device, dt):
+    M, P = 11, [8] * 5
+    X, Fs = case(M, P, P, dt, "srand", 2)
+    ref = oracle.alg1(X, Fs)
+    den = oracle.alg1(np.abs(X), [np.abs(f) for f in Fs])  # (|X| . (x)|F|)
+    Y = run(kron, X, Fs, cuda_device)
+    assert float(np.max(np.abs(Y - ref) / den)) <= TOL[dt]
+
+
+def test_identity_and_permutation_factors(kron, cuda_device):
+    rng = np.random.default_rng(3)
+    P = [8, 8, 8, 8]
+    X = synth.matrix(19, 8 ** 4, synth.SEED_BASE, 0, "urand", np.float32)
+    Y = run(kron, X, [np.eye(8, dtype=np.float32)] * 4, cuda_device)
+    assert np.array_equal(Y, X)
+    perms = [rng.permutation(8) for _ in P]
+    Fs = [np.eye(8, dtype=np.float32)[p] for p in perms]
+    Y = run(kron, X, Fs, cuda_device)
+    assert np.array_equal(Y, oracle.alg1(X, Fs).astype(np.float32))  # a pure column permutation
+
+
+def test_m_zero_and_empty(kron, cuda_device):
+    import torch
+    X = torch.empty((0, 64), dtype=torch.float32, device=cuda_device)
+    F = [torch.eye(8, device=cuda_device)] * 2
+    Y = kron.matmul(X, F)
+    assert Y.shape == (0, 64)
+
+
+def test_workspace_variant_and_stream(kron, cuda_device):
+    import torch
+    X, Fs = case(64, [8] * 6, [8] * 6, np.float32, "urand", 3)
+    Xd, Fd = to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs]
+    ws = torch.empty(kron.workspace_size(64, [8] * 6, [8] * 6, torch.float32), dtype=torch.uint8, device=cuda_device)
+    out = torch.empty((64, 8 ** 6), dtype=torch.float32, device=cuda_device)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        kron.matmul_ws(Xd, Fd, out, ws)
+    s.synchronize()
+    assert rel_err(out.cpu().numpy(), oracle.alg1(X, Fs)) <= 1e-5
+    with pytest.raises(kron.KronError):
+        kron.matmul_ws(Xd, Fd, out, ws[:10])  # workspace too small -> KRON_ERR_SHAPE, nothing enqueued
+
+
+# ------------------------------------------------------------------ full BASELINE sizes, sampled rows
+
+FULL = [
+    ("B", 1, 1024, [8] * 6, [8] * 6, np.float32),
+    ("C32", 2, 1024, [32] * 4, [32] * 4, np.float32),
+    ("C64", 2, 1024, [32] * 4, [32] * 4, np.float64),
+    ("D1", 3, 320, [128] * 3, [128] * 3, np.float64),
+    ("D2", 4, 320, [64] * 3, [32] * 3, np.float64),
+    ("E", 5, 4096, [16] * 5, [16] * 5, np.float32),
+]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name,cfg,M,P,Q,dt", FULL)
+def test_full_size_sampled_rows(kron, cuda_device, name, cfg, M, P, Q, dt):
+    import torch
+    seed = synth.SEED_BASE + cfg
+    K, L = int(np.prod(P)), int(np.prod(Q))
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    X = torch.empty((M, K), dtype=tdt, device=cuda_device)
+    synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", dt)
+    Fs_h = synth.factors(P, Q, seed, "urand", dt)
+    Y = kron.matmul(X, [to_dev(f, cuda_device) for f in Fs_h])
+    rows = synth.row_subset(M, extra=12)
+    Ys = Y[torch.from_numpy(rows).to(cuda_device)].cpu().numpy()
+    del X, Y
+    torch.cuda.empty_cache()
+    ref = oracle.alg1(synth.rows_of(rows, K, seed, 0, "urand"), Fs_h)
+    assert rel_err(Ys, ref) <= TOL[dt]
