@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""bench.py — Kron-Matmul throughput on B200 (BASELINE.json metric: "Kron-Matmul GFLOP/s and % roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config B] [--impl ours|reference]
+
+A step is one whole Kron-Matmul Y = X·(F^1 ⊗ … ⊗ F^N) over the configuration's full M rows (all passes
+of the plan).  Default workload: config B (BASELINE.json configs[1]: M=1024, 6 factors 8x8, fp32).
+FLOPs are the method's algorithmic count sum_f 2·M·W_f·Q_f (north_star).
+
+Timing: W untimed warm-ups, then exactly K steps on the device between CUDA events on the launching
+stream, bracketed by barrier + synchronize, max over ranks.  Inputs (>= 1 GiB) are larger than the
+126 MB L2, so no flush is needed.  Clocks and throttle reasons are sampled with NVML during the
+timed region.  Per-pass CUDA events (kron_matmul_ws_events) give the dominant kernel's average
+launch time for the roofline object.
+
+N > 1 (torchrun, one rank per GPU): every rank runs the configuration on its own block of rows of
+a taller X (row partition: no communication) -> "scaling": "weak".
+
+--impl reference times the CPU oracle (oracle/, plain C fp64 Algorithm 1) on the host cores, each
+step a bounded row sample of the same workload (this tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Kron-Matmul GFLOP/s and % roofline at 1/2/4/8 B200, fp32 and fp64"
+
+CONFIGS = {
+    # name: (cfg index for the seed, M, P, Q, dtype)
+    "A": (0, 16, [4] * 2, [4] * 2, "float32"),
+    "B": (1, 1024, [8] * 6, [8] * 6, "float32"),
+    "C32": (2, 1024, [32] * 4, [32] * 4, "float32"),
+    "C64": (2, 1024, [32] * 4, [32] * 4, "float64"),
+    "D1": (3, 320, [128] * 3, [128] * 3, "float64"),
+    "D2": (4, 320, [64] * 3, [32] * 3, "float64"),
+    "E": (5, 4096, [16] * 5, [16] * 5, "float32"),
+}
+
+# ALU peaks derived from the B200 unit counts:
+# 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz; FP64 = half the FP32 lanes.
+FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FP64_PEAK_TFLOPS = FP32_PEAK_TFLOPS / 2
+HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
+
+REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+           0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting", 0x100: "display_clock_setting"}
+
+
+def widths(P, Q):
+    N = len(P)
+    W = [0] * (N + 1)
+    W[N] = int(np.prod(P))
+    for f in range(N, 0, -1):
+        W[f - 1] = W[f] // P[f - 1] * Q[f - 1]
+    return W
+
+
+def flops_of(M, P, Q):
+    W = widths(P, Q)
+    return float(sum(2.0 * M * W[f] * Q[f - 1] for f in range(1, len(P) + 1)))
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config, kernel_prefix):
+    """dram read+write bytes per launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(config, {}).get(kernel_prefix)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """NVML sampling of SM clock + throttle reasons during the timed region."""
+
+    def __init__(self, dev_index, period=0.01):
+        self.samples, self.reasons, self.period = [], 0, period
+        self.stop_flag = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+        try:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            self.reasons |= nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+
+    def _run(self):
+        while not self.stop_flag.is_set():
+            self._sample()
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._sample()
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self.stop_flag.set()
+            self.t.join()
+            self._sample()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        names = [n for bit, n in REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_oracle_rate(M, P, Q, seed, dt, target_s=8.0, max_rows=None):
+    """Oracle GFLOP/s on a bounded row sample (rows are independent in Algorithm 1)."""
+    import oracle
+    import synth
+    K = int(np.prod(P))
+    Fs = synth.factors(P, Q, seed, "urand", dt)
+    per_row = flops_of(1, P, Q)
+    rows = 1
+    t = 0.0
+    while True:
+        Xr = synth.rows_of(np.arange(rows), K, seed, 0, "urand").astype(dt)
+        t0 = time.perf_counter()
+        oracle.alg1(Xr, Fs)
+        t = time.perf_counter() - t0
+        cap = max_rows or M
+        if t >= target_s / 4 or rows >= cap:
+            break
+        rows = min(cap, max(rows * 2, int(rows * target_s / 4 / max(t, 1e-3))))
+    return per_row * rows / t / 1e9, rows, t
+
+
+def run_reference(args, cfg_name):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    cfg, M, P, Q, dtn = CONFIGS[cfg_name]
+    import oracle
+    import synth
+    dt = np.float32 if dtn == "float32" else np.float64
+    seed = synth.SEED_BASE + cfg
+    K = int(np.prod(P))
+    cores = len(os.sched_getaffinity(0))
+    per_row = flops_of(1, P, Q)
+    # rows per step: ~0.15 s of oracle work at ~1 GFLOP/s/core
+    rows = int(max(1, min(M, 0.15 * cores * 1e9 / per_row)))
+    Fs = synth.factors(P, Q, seed, "urand", dt)
+    Xr = synth.rows_of(np.arange(rows), K, seed, 0, "urand").astype(dt)
+    for _ in range(args.warmup):
+        oracle.alg1(Xr, Fs)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.alg1(Xr, Fs)
+    el = time.perf_counter() - t0
+    value = per_row * rows * args.steps / el / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded counter-based U[0,1))",
+        "config": {"workload": cfg_name, "M": M, "P": P, "Q": Q, "input_dtype": dtn, "rows_per_step": rows},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "sample": f"rows 0..{rows - 1} of config {cfg_name} (M={M}) per step; plain C fp64 "
+                                   f"Algorithm 1, OpenMP over rows"},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+
+    if args.impl == "reference":
+        return run_reference(args, args.config)
+
+    import torch
+    import synth
+    from paper_2401_10187_b200 import kron
+
+    ws, rank, local = dist_env()
+    if ws != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    cfg, M, P, Q, dtn = CONFIGS[args.config]
+    dt = np.float32 if dtn == "float32" else np.float64
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    es = 4 if dt == np.float32 else 8
+    seed = synth.SEED_BASE + cfg
+    K, L = int(np.prod(P)), int(np.prod(Q))
+    stream = torch.cuda.current_stream()
+
+    # inputs resident in HBM: this rank's block of rows of a (ws*M) x K matrix
+    X = torch.empty((M, K), dtype=tdt, device=dev)
+    synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=rank * M, ld=K)
+    Fs_h = synth.factors(P, Q, seed, "urand", dt)
+    Fs = [torch.from_numpy(f).to(dev) for f in Fs_h]
+    Y = torch.empty((M, L), dtype=tdt, device=dev)
+    wsz = kron.workspace_size(M, P, Q, tdt)
+    work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
+    plan = kron.plan_describe(M, P, Q, tdt)
+    npass = len(plan)
+    W = widths(P, Q)
+
+    def mk_events(n):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in evs:
+            e.record(stream)  # materialise the cudaEvent_t handles
+        return evs
+
+    for _ in range(args.warmup):
+        kron.matmul_ws(X, Fs, Y, work)
+    torch.cuda.synchronize()
+
+    pass_events = [mk_events(npass + 1) for _ in range(args.steps)]
+    t_start, t_end = mk_events(2)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        t_start.record(stream)
+        for k in range(args.steps):
+            kron.matmul_ws_events(X, Fs, Y, work, [e.cuda_event for e in pass_events[k]])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = t_start.elapsed_time(t_end)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    fl_step = flops_of(M, P, Q)
+    value = ws * fl_step * args.steps / (ms / 1e3) / 1e9  # whole-job GFLOP/s
+
+    # per-pass (kernel) timing -> roofline of the dominant kernel
+    pass_ms = np.zeros(npass)
+    for k in range(args.steps):
+        for i in range(npass):
+            pass_ms[i] += pass_events[k][i].elapsed_time(pass_events[k][i + 1])
+    pass_ms /= args.steps
+    dom = int(np.argmax(pass_ms))
+    first, nf, kind = plan[dom]
+    w_in, w_out = W[first], W[first - nf]
+    alg_bytes = es * M * (w_in + w_out) + sum(es * P[f - 1] * Q[f - 1] for f in range(first, first - nf, -1))
+    alg_flops = sum(2.0 * M * W[f] * Q[f - 1] for f in range(first, first - nf, -1))
+    hbm_peak, hbm_src = measured_peaks()
+    alu_peak = FP32_PEAK_TFLOPS if dt == np.float32 else FP64_PEAK_TFLOPS
+    t_dom = pass_ms[dom] / 1e3
+    t_hbm, t_alu = alg_bytes / (hbm_peak * 1e9), alg_flops / (alu_peak * 1e12)
+    if t_hbm >= t_alu:
+        ach = alg_bytes / t_dom / 1e9
+        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src}
+    else:
+        ach = alg_flops / t_dom / 1e12
+        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
+                "frac": round(ach / alu_peak, 4),
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")}
+    kname = {"fused": "kron_fused_kernel", "generic": "sliced_generic_kernel", "gemm": "kron_gemm"}[kind]
+    roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
+                 "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
+                 "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
+                 "traffic": ncu_traffic(args.config, kname)})
+
+    # whole-step roofline (all passes): T_roof = max(B_alg/BW, F_alg/peak)
+    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt)
+    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12))
+    step_frac = t_roof / (ms / args.steps / 1e3)
+
+    # e2e through the public API with host buffers: H2D of X and F, kron_matmul, D2H of Y
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((M, K), dtype=tdt, pin_memory=True)
+        Xh.numpy().reshape(-1)[:] = synth.fill(M * K, seed, 0, "urand", dt, first=rank * M * K)
+        Fh = [torch.from_numpy(f).pin_memory() for f in Fs_h]
+        Yh = torch.empty((M, L), dtype=tdt, pin_memory=True)
+        del X
+        torch.cuda.empty_cache()
+        Xd = torch.empty((M, K), dtype=tdt, device=dev)
+        Fd = [torch.empty_like(f, device=dev) for f in Fh]
+        Yd = torch.empty((M, L), dtype=tdt, device=dev)
+
+        def e2e_step():
+            Xd.copy_(Xh, non_blocking=True)
+            for a, b in zip(Fd, Fh):
+                a.copy_(b, non_blocking=True)
+            kron.matmul(Xd, Fd, out=Yd)
+            Yh.copy_(Yd, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        e0, e1 = mk_events(2)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if ws > 1:
+            t = torch.tensor([ems], dtype=torch.float64, device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ems = float(t.item())
+        h2d = M * K * es + sum(f.numel() * es for f in Fh)
+        e2e = {"value": round(ws * fl_step * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(M * L * es), "steps": args.e2e_steps,
+               "path": "pinned host X,F -> kron_matmul (public C-ABI) -> pinned host Y"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        rate, rows, t = cpu_oracle_rate(M, P, Q, seed, dt)
+        cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"rows 0..{rows - 1} of config {args.config} (M={M}), {t:.1f} s; plain C fp64 "
+                         f"Algorithm 1 (oracle/), OpenMP over rows"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+            "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
+            "config": {"workload": args.config, "M_per_gpu": M, "P": P, "Q": Q, "K": K, "L": L,
+                       "plan": [list(p) for p in plan],
+                       "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "roofline": roof,
+            "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(step_frac, 4),
+                              "alg_bytes": b_alg, "alg_flops": f_alg},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": npass * args.steps,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

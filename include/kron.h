@@ -72,6 +72,13 @@ kron_status_t kron_matmul_ws(int64_t M, int32_t N, const int32_t *P, const int32
                              const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
                              size_t workspace_bytes, void *stream);
 
+/* kron_matmul_ws with per-pass timing hooks (used by bench.py's roofline): events[i] (cudaEvent_t
+ * handles passed as void*) is recorded on `stream` right before pass i is launched and
+ * events[npasses] after the last pass; nevents must be >= npasses + 1 (KRON_ERR_INVALID_ARG).     */
+kron_status_t kron_matmul_ws_events(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                                    const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                                    size_t workspace_bytes, void *const *events, int32_t nevents, void *stream);
+
 /* ---------------------------------------------------------------------------------------------
  * Planner introspection (host only; no GPU needed).  Describes the pass plan kron_matmul uses:
  * pass i applies factors F^{first[i]}, F^{first[i]-1}, ..., F^{first[i]-nfactors[i]+1}

@@ -100,14 +100,18 @@ kron_status_t cached_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, 
   return KRON_OK;
 }
 
-kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream) {
+kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
+                       void *const *events = nullptr) {
   const size_t es = es_of(plan.dtype);
+  int ip = 0;
   void *bufs[4] = {const_cast<void *>(X), Y, ws,
                    ws ? static_cast<char *>(ws) + (size_t)plan.ws_elems * es : nullptr};
   for (const PassPlan &pp : plan.passes) {
     const void *in = bufs[pp.src];
     void *out = bufs[pp.dst];
     int err = 0;
+    if (events && cudaEventRecord((cudaEvent_t)events[ip], (cudaStream_t)stream) != cudaSuccess) return KRON_ERR_CUDA;
+    ++ip;
     if (pp.kind == KIND_FUSED) {
       if (!tmap_available()) return KRON_ERR_CUDA;
       const void *grp[kMaxFused];
@@ -120,6 +124,7 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
     }
     if (err != 0) return KRON_ERR_CUDA;
   }
+  if (events && cudaEventRecord((cudaEvent_t)events[ip], (cudaStream_t)stream) != cudaSuccess) return KRON_ERR_CUDA;
   return KRON_OK;
 }
 
@@ -274,6 +279,24 @@ kron_status_t kron_matmul_ws(int64_t M, int32_t N, const int32_t *P, const int32
   const size_t need = ws_bytes_of(*plan);
   if (need > 0 && (!workspace || workspace_bytes < need)) return KRON_ERR_SHAPE;
   return run_plan(*plan, X, F, Y, workspace, stream);
+}
+
+kron_status_t kron_matmul_ws_events(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                                    const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                                    size_t workspace_bytes, void *const *events, int32_t nevents, void *stream) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X || !F || !Y || !events) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> plan;
+  st = cached_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  if (nevents < (int32_t)plan->passes.size() + 1) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < (int)plan->passes.size() + 1; ++i)
+    if (!events[i]) return KRON_ERR_INVALID_ARG;
+  const size_t need = ws_bytes_of(*plan);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return KRON_ERR_SHAPE;
+  return run_plan(*plan, X, F, Y, workspace, stream, events);
 }
 
 kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,

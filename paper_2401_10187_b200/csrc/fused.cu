@@ -50,6 +50,96 @@ struct FusedArgs {
 
 namespace {
 
+template <typename T, int P, int RS>
+struct SliceRegs {
+  T x[RS][P];
+};
+
+// Loads RS whole slices (P contiguous elements each) from shared memory; offs are byte offsets of
+// the 16-byte (or smaller) vectors, already swizzled.
+template <typename T, int P, int RS, int NV, int VB>
+__device__ __forceinline__ void load_slices(const unsigned char *buf, const uint32_t (&offs)[RS][NV],
+                                            const bool (&act)[RS], T (&x)[RS][P]) {
+  constexpr int ES = sizeof(T), EPV = VB / ES;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const unsigned char *src = buf + offs[r][v];
+      if (act[r]) {
+        if constexpr (VB == 16 && ES == 4) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(src);
+          x[r][v * EPV + 0] = t4.x; x[r][v * EPV + 1] = t4.y; x[r][v * EPV + 2] = t4.z; x[r][v * EPV + 3] = t4.w;
+        } else if constexpr (VB == 16 && ES == 8) {
+          const double2 t2 = *reinterpret_cast<const double2 *>(src);
+          x[r][v * EPV + 0] = t2.x; x[r][v * EPV + 1] = t2.y;
+        } else if constexpr (VB == 8 && ES == 4) {
+          const float2 t2 = *reinterpret_cast<const float2 *>(src);
+          x[r][v * EPV + 0] = t2.x; x[r][v * EPV + 1] = t2.y;
+        } else {
+          x[r][v] = *reinterpret_cast<const T *>(src);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) x[r][v * EPV + e] = T(0);
+      }
+    }
+  }
+}
+
+// One sliced multiply of the register-resident slices with the factor Fst (shared, [p][q]) and the
+// in-place store of out[row][q*Sl + s].  SWZ: 0 linear layout (last step, TMA-store source),
+// 1 swizzled with the q-stride a multiple of 1024 B (swizzle commutes with +q*stride), 2 general.
+template <typename T, int P, int RS, int SWZ>
+__device__ __forceinline__ void multiply_store(unsigned char *buf, const T *Fst, const T (&x)[RS][P],
+                                               const uint32_t (&wb)[RS], const bool (&act)[RS], uint32_t strideQ) {
+  constexpr int ES = sizeof(T);
+  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;  // factor columns per broadcast group
+  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
+  constexpr int FNV = QB * ES / FVB;
+  constexpr int FEPV = FVB / ES;
+#pragma unroll
+  for (int q0 = 0; q0 < P; q0 += QB) {
+    T acc[RS][QB];
+#pragma unroll
+    for (int r = 0; r < RS; ++r)
+#pragma unroll
+      for (int j = 0; j < QB; ++j) acc[r][j] = T(0);
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      T f[QB];
+      const T *fp = Fst + p * P + q0;
+#pragma unroll
+      for (int v = 0; v < FNV; ++v) {
+        if constexpr (FVB == 16 && ES == 4) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
+        } else if constexpr (FVB == 16 && ES == 8) {
+          const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+#pragma unroll
+        for (int j = 0; j < QB; ++j) acc[r][j] = fma(x[r][p], f[j], acc[r][j]);
+    }
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      if (!act[r]) continue;
+#pragma unroll
+      for (int j = 0; j < QB; ++j) {
+        uint32_t off = wb[r] + (uint32_t)(q0 + j) * strideQ;
+        if constexpr (SWZ == 2) off = swz128(off);
+        *reinterpret_cast<T *>(buf + off) = acc[r][j];
+      }
+    }
+  }
+}
+
 template <typename T, int P, int RS, int NT>
 __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                        const __grid_constant__ CUtensorMap tm_out,
@@ -58,15 +148,12 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
   constexpr int SLICE_BYTES = P * ES;
   constexpr int VB = SLICE_BYTES < 16 ? SLICE_BYTES : 16;  // bytes per shared-memory vector access
   constexpr int NV = SLICE_BYTES / VB;                      // vector loads per slice
-  constexpr int EPV = VB / ES;                              // elements per vector
-  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;          // factor columns per broadcast group
-  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
-  constexpr int FNV = QB * ES / FVB;
-  constexpr int FEPV = FVB / ES;
   constexpr int LINE = 128 / ES;
 
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char *base = reinterpret_cast<unsigned char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // Shared memory: [stages x stage_bytes (1024-aligned, 128B-swizzled tiles)] [factors] [mbarriers].
+  // Offsets stay derived from the __shared__ array so every access is LDS/STS.
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   T *Fs = reinterpret_cast<T *>(base + (size_t)a.stages * a.stage_bytes);
   uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(Fs) +
                                                 ((a.nf * P * P * ES + 15) & ~15));
@@ -83,6 +170,22 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
     prefetch_tmap(&tm_in);
     prefetch_tmap(&tm_out);
   }
+
+  // Per-thread slice bookkeeping: identical for every tile (same tile geometry).
+  bool act[RS];
+  uint32_t rd[RS][NV], wlin[RS], wswz[RS];
+  const uint32_t strideQ = (uint32_t)a.Sl * ES;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const int sl = tid + r * NT;
+    act[r] = sl < a.nslices;
+    const int row = sl / a.Sl, s = sl - row * a.Sl;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) rd[r][v] = swz128((uint32_t)sl * SLICE_BYTES + v * VB);
+    wlin[r] = ((uint32_t)row * a.tileK + (uint32_t)s) * ES;
+    wswz[r] = swz128(wlin[r]);
+  }
+  const bool fast_swz = (strideQ & 1023u) == 0;
   __syncthreads();
 
   auto issue_load = [&](int it) {
@@ -107,98 +210,19 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
     mbar_wait(&bars[st], (uint32_t)((it / a.stages) & 1));
     unsigned char *buf = base + (size_t)st * a.stage_bytes;
 
-    int row[RS], sidx[RS];
-    bool act[RS];
-#pragma unroll
-    for (int r = 0; r < RS; ++r) {
-      const int sl = tid + r * NT;
-      act[r] = sl < a.nslices;
-      row[r] = sl / a.Sl;
-      sidx[r] = sl - row[r] * a.Sl;
-    }
-
     for (int step = 0; step < a.nf; ++step) {
       const T *Fst = Fs + step * P * P;
-      const bool last = step == a.nf - 1;
-      // ---- read my slices (swizzled layout) into registers
       T x[RS][P];
-#pragma unroll
-      for (int r = 0; r < RS; ++r) {
-        const uint32_t b0 = (uint32_t)(tid + r * NT) * SLICE_BYTES;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-          if (act[r]) {
-            const unsigned char *src = buf + swz128(b0 + v * VB);
-            if constexpr (VB == 16) {
-              if constexpr (ES == 4) {
-                const float4 t4 = *reinterpret_cast<const float4 *>(src);
-                x[r][v * EPV + 0] = t4.x; x[r][v * EPV + 1] = t4.y; x[r][v * EPV + 2] = t4.z; x[r][v * EPV + 3] = t4.w;
-              } else {
-                const double2 t2 = *reinterpret_cast<const double2 *>(src);
-                x[r][v * EPV + 0] = t2.x; x[r][v * EPV + 1] = t2.y;
-              }
-            } else if constexpr (VB == 8) {
-              if constexpr (ES == 4) {
-                const float2 t2 = *reinterpret_cast<const float2 *>(src);
-                x[r][v * EPV + 0] = t2.x; x[r][v * EPV + 1] = t2.y;
-              } else {
-                x[r][v] = *reinterpret_cast<const double *>(src);
-              }
-            } else {
-              x[r][v] = *reinterpret_cast<const T *>(src);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < EPV; ++e) x[r][v * EPV + e] = T(0);
-          }
-        }
-      }
+      load_slices<T, P, RS, NV, VB>(buf, rd, act, x);  // a4: my slices -> registers
       __syncthreads();  // every slice of this step is in registers: the tile may be overwritten
-      // ---- multiply and write the outputs in place: out[row][q*Sl + s]
-#pragma unroll
-      for (int q0 = 0; q0 < P; q0 += QB) {
-        T acc[RS][QB];
-#pragma unroll
-        for (int r = 0; r < RS; ++r)
-#pragma unroll
-          for (int j = 0; j < QB; ++j) acc[r][j] = T(0);
-#pragma unroll
-        for (int p = 0; p < P; ++p) {
-          T f[QB];
-          const T *fp = Fst + p * P + q0;
-#pragma unroll
-          for (int v = 0; v < FNV; ++v) {
-            if constexpr (FVB == 16) {
-              if constexpr (ES == 4) {
-                const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
-                f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
-              } else {
-                const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
-                f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
-            }
-          }
-#pragma unroll
-          for (int r = 0; r < RS; ++r)
-#pragma unroll
-            for (int j = 0; j < QB; ++j) acc[r][j] = fma(x[r][p], f[j], acc[r][j]);
-        }
-#pragma unroll
-        for (int r = 0; r < RS; ++r) {
-          if (!act[r]) continue;
-          const uint32_t e0 = (uint32_t)row[r] * a.tileK + (uint32_t)sidx[r];
-#pragma unroll
-          for (int j = 0; j < QB; ++j) {
-            uint32_t off = (e0 + (uint32_t)(q0 + j) * a.Sl) * ES;
-            if (!last) off = swz128(off);
-            *reinterpret_cast<T *>(buf + off) = acc[r][j];
-          }
-        }
+      if (step == a.nf - 1) {
+        multiply_store<T, P, RS, 0>(buf, Fst, x, wlin, act, strideQ);  // a6 source: linear layout
+        fence_proxy_async_smem();
+      } else if (fast_swz) {
+        multiply_store<T, P, RS, 1>(buf, Fst, x, wswz, act, strideQ);  // a5: swizzled for the next step
+      } else {
+        multiply_store<T, P, RS, 2>(buf, Fst, x, wlin, act, strideQ);
       }
-      if (last) fence_proxy_async_smem();
       __syncthreads();
     }
     if (tid == 0) {
@@ -218,7 +242,7 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
 
 const FusedInstance kInstances[] = {
     // dtype, P, NT, RS
-    {KRON_F32, 2, 256, 8},  {KRON_F32, 4, 256, 4},  {KRON_F32, 8, 256, 2},
+    {KRON_F32, 2, 256, 8},  {KRON_F32, 4, 256, 4},  {KRON_F32, 8, 128, 4},
     {KRON_F32, 16, 256, 2}, {KRON_F32, 32, 128, 2}, {KRON_F64, 2, 256, 4},
     {KRON_F64, 4, 256, 2},  {KRON_F64, 8, 256, 1},  {KRON_F64, 16, 128, 2},
     {KRON_F64, 32, 128, 1},
@@ -231,7 +255,7 @@ KernelFn instance_kernel(int i) {
   switch (i) {
     case 0: return kron_fused_kernel<float, 2, 8, 256>;
     case 1: return kron_fused_kernel<float, 4, 4, 256>;
-    case 2: return kron_fused_kernel<float, 8, 2, 256>;
+    case 2: return kron_fused_kernel<float, 8, 4, 128>;
     case 3: return kron_fused_kernel<float, 16, 2, 256>;
     case 4: return kron_fused_kernel<float, 32, 2, 128>;
     case 5: return kron_fused_kernel<double, 2, 4, 256>;

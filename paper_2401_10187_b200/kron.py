@@ -29,6 +29,10 @@ _lib.kron_matmul.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctype
 _lib.kron_matmul_ws.restype = ctypes.c_int
 _lib.kron_matmul_ws.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
                                 ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+_lib.kron_matmul_ws_events.restype = ctypes.c_int
+_lib.kron_matmul_ws_events.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp,
+                                       ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, _vpp,
+                                       ctypes.c_int32, ctypes.c_void_p]
 _lib.kron_matmul_workspace_size.restype = ctypes.c_int
 _lib.kron_matmul_workspace_size.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int,
                                             ctypes.POINTER(ctypes.c_size_t)]
@@ -169,6 +173,21 @@ def matmul_ws(X, Fs, out, workspace, stream=None):
     wbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     _check(_lib.kron_matmul_ws(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype),
                                wptr, wbytes, _stream_ptr(stream)), "kron_matmul_ws")
+    return out
+
+
+def matmul_ws_events(X, Fs, out, workspace, events, stream=None):
+    """kron_matmul_ws_events(): like matmul_ws, recording events[i] (raw cudaEvent_t handles) before
+    pass i and events[npasses] after the last pass, for per-kernel timing."""
+    P, Q = _prep(X, Fs)
+    Pa, Qa = _shape_arrays(P, Q)
+    Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
+    Ev = (ctypes.c_void_p * len(events))(*[int(e) for e in events])
+    wptr = workspace.data_ptr() if workspace is not None else None
+    wbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    _check(_lib.kron_matmul_ws_events(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(),
+                                      dtype_code(X.dtype), wptr, wbytes, Ev, len(events), _stream_ptr(stream)),
+           "kron_matmul_ws_events")
     return out
 
 
