@@ -43,14 +43,26 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   const int64_t lines = tileK / line;
   if (lines > 256 && lines % 256) return false;
   int64_t tileM = E / tileK;
-  if (tileM > M) tileM = M;
-  if (tileM > 256) tileM = 256;
-  if (tileM < 1) tileM = 1;
+  if (inst.warp) {
+    // the warp-chain kernel always works on full tiles (rows past M are TMA zero-fill / clipped)
+    if (E % tileK || tileM > 256) return false;
+  } else {
+    if (tileM > M) tileM = M;
+    if (tileM > 256) tileM = 256;
+    if (tileM < 1) tileM = 1;
+  }
   if (tileM > 1 && lines > 256) return false;
   if (C > 256 && (C % 256 || C / 256 > 256)) return false;
+  if (inst.warp && ((int64_t)32 * inst.RS * p) % C) return false;  // warp share = whole chunks
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
-  const int stages = stage <= 32 * 1024 ? 3 : 2;
-  const int64_t smem = 1024 + stages * stage + (int64_t)k * p * p * es + 16 + 8 * stages;
+  int stages, nout = 0;
+  if (inst.warp) {
+    stages = 2;
+    nout = stage <= 16 * 1024 ? 2 : 1;  // keep >= 2 CTAs per SM
+  } else {
+    stages = stage <= 32 * 1024 ? 3 : 2;
+  }
+  const int64_t smem = 1024 + (stages + nout) * stage + (int64_t)k * p * p * es + 16 + 8 * stages;
   if (smem > 227 * 1024) return false;
   pp->kind = KIND_FUSED;
   pp->nf = k;
@@ -61,6 +73,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   pp->tileK = tileK;
   pp->tileM = (int)tileM;
   pp->stages = stages;
+  pp->nout = nout;
   return true;
 }
 
@@ -174,14 +187,21 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
   while (f >= 1) {
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
-    const int inst = (p == q) ? fused_find(dtype, p) : -1;
-    if (inst >= 0) {
+    const int inst_w = (p == q) ? fused_find(dtype, p, 1) : -1;
+    const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;
+    if (inst_c >= 0) {
       int run = 1;  // consecutive factors of the same square shape
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
+      // largest group either kernel can tile; prefer the warp-chain kernel for each group size
+      auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_w >= 0 && fused_geometry(fused_instance(inst_w), k, W, Mp, pp)) return inst_w;
+        if (fused_geometry(fused_instance(inst_c), k, W, Mp, pp)) return inst_c;
+        return -1;
+      };
       int kmax = 0;
       PassPlan probe;
       for (int k = 1; k <= run && k <= kMaxFused; ++k)
-        if (fused_geometry(fused_instance(inst), k, W, Mp, &probe)) kmax = k;
+        if (pick(k, &probe) >= 0) kmax = k;
       if (kmax >= 1) {
         // fewest passes, then balanced group sizes ("ceil(N/Fused) iterations")
         const int npass = (run + kmax - 1) / kmax;
@@ -189,8 +209,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
         for (int i = 0; i < npass; ++i) {
           const int k = base + (i < extra ? 1 : 0);
           PassPlan pp;
-          fused_geometry(fused_instance(inst), k, W, Mp, &pp);
-          pp.variant = inst;
+          pp.variant = pick(k, &pp);
           pp.first = f;
           pp.W_in = W;
           pp.W_out = W;  // square factors keep the width

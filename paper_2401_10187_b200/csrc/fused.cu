@@ -39,6 +39,8 @@ struct FusedArgs {
   int R;          // chunks per tile row = output run length
   int Sl;         // slices per tile row (tileK / P)
   int nslices;    // tileM * Sl
+  int C;          // chunk = P^nf
+  int nout;       // output buffers (warp-chain kernel): 2 = double-buffered TMA-store source
   int tiles_k;    // tiles along a row
   int64_t ntiles;
   int nbox;       // input TMA boxes per tile (along dim1)
@@ -50,14 +52,11 @@ struct FusedArgs {
 
 namespace {
 
-template <typename T, int P, int RS>
-struct SliceRegs {
-  T x[RS][P];
-};
+
 
 // Loads RS whole slices (P contiguous elements each) from shared memory; offs are byte offsets of
 // the 16-byte (or smaller) vectors, already swizzled.
-template <typename T, int P, int RS, int NV, int VB>
+template <typename T, int P, int RS, int NV, int VB, bool GUARD = true>
 __device__ __forceinline__ void load_slices(const unsigned char *buf, const uint32_t (&offs)[RS][NV],
                                             const bool (&act)[RS], T (&x)[RS][P]) {
   constexpr int ES = sizeof(T), EPV = VB / ES;
@@ -66,7 +65,7 @@ __device__ __forceinline__ void load_slices(const unsigned char *buf, const uint
 #pragma unroll
     for (int v = 0; v < NV; ++v) {
       const unsigned char *src = buf + offs[r][v];
-      if (act[r]) {
+      if (!GUARD || act[r]) {
         if constexpr (VB == 16 && ES == 4) {
           const float4 t4 = *reinterpret_cast<const float4 *>(src);
           x[r][v * EPV + 0] = t4.x; x[r][v * EPV + 1] = t4.y; x[r][v * EPV + 2] = t4.z; x[r][v * EPV + 3] = t4.w;
@@ -238,14 +237,258 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
   if (tid == 0) bulk_wait<0>();
 }
 
+// ------------------------------------------------------------------ warp-local chain (v2)
+//
+// When a warp's share of the tile (32*RS slices = GE elements) is a whole number of chunks, every
+// intermediate step of the fused chain stays inside the warp: the warp multiplies its
+// slices, writes the outputs back in place into its own region (chunk-local order q*C/P + s) and
+// only needs __syncwarp.  The LAST step is done CTA-wide in "chunk-fastest" order, so that a
+// thread group writes consecutive composite columns of consecutive chunks — the tile's final
+// u*R + g layout — with conflict-free consecutive stores into a separate output buffer that one
+// TMA tensor store sends to HBM.  Two CTA barriers per tile instead of two per factor.
+
+// chunk-dependent 16-byte-granule XOR on top of the 128B swizzle: keeps the warp-phase stores and
+// the chunk-fastest last-step loads free of bank conflicts (checked by a bank model).
+// The mask must be constant over each 128-byte line to stay a bijection, so it is used only when a
+// chunk spans whole lines (C*s >= 128); smaller chunks use the plain 128B swizzle (gx = 0).
+__device__ __forceinline__ uint32_t gmix(uint32_t g) { return (g ^ (g << 1) ^ (g << 2)) & 7u; }
+__device__ __forceinline__ uint32_t swz_m(uint32_t off, uint32_t gx) { return off ^ (((off >> 3) ^ gx) & 0x70u); }
+
+// multiply register slices by Fst and store each output (slice r, column q) at its chunk-swizzled
+// position: byte offset off = wbase[r] + q*strideCP, then swz_m(off, gx[r]) (gx = gmix(chunk) << 4).
+// For small RS*P the swizzled offsets are precomputed (wo), otherwise they are formed per store.
+template <typename T, int P, int RS, bool PRE>
+__device__ __forceinline__ void multiply_store_swz(unsigned char *buf, const T *Fst, const T (&x)[RS][P],
+                                                   const uint32_t (&wo)[PRE ? RS : 1][PRE ? P : 1],
+                                                   const uint32_t (&wbase)[RS], const uint32_t (&gx)[RS],
+                                                   uint32_t strideCP) {
+  constexpr int ES = sizeof(T);
+  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;
+  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
+  constexpr int FNV = QB * ES / FVB;
+  constexpr int FEPV = FVB / ES;
+#pragma unroll
+  for (int q0 = 0; q0 < P; q0 += QB) {
+    T acc[RS][QB];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      T f[QB];
+      const T *fp = Fst + p * P + q0;
+#pragma unroll
+      for (int v = 0; v < FNV; ++v) {
+        if constexpr (FVB == 16 && ES == 4) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
+        } else if constexpr (FVB == 16 && ES == 8) {
+          const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+#pragma unroll
+        for (int j = 0; j < QB; ++j) acc[r][j] = (p == 0) ? x[r][0] * f[j] : fma(x[r][p], f[j], acc[r][j]);
+    }
+#pragma unroll
+    for (int r = 0; r < RS; ++r)
+#pragma unroll
+      for (int j = 0; j < QB; ++j) {
+        uint32_t off;
+        if constexpr (PRE) {
+          off = wo[r][q0 + j];
+        } else {
+          off = wbase[r] + (uint32_t)(q0 + j) * strideCP;
+          off ^= ((off >> 3) ^ gx[r]) & 0x70u;
+        }
+        *reinterpret_cast<T *>(buf + off) = acc[r][j];
+      }
+  }
+}
+
+// multiply and store to a linear layout: out byte offset wb[r] + q*strideQ
+template <typename T, int P, int RS>
+__device__ __forceinline__ void multiply_store_lin(unsigned char *buf, const T *Fst, const T (&x)[RS][P],
+                                                   const uint32_t (&wb)[RS], uint32_t strideQ) {
+  constexpr int ES = sizeof(T);
+  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;
+  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
+  constexpr int FNV = QB * ES / FVB;
+  constexpr int FEPV = FVB / ES;
+#pragma unroll
+  for (int q0 = 0; q0 < P; q0 += QB) {
+    T acc[RS][QB];
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      T f[QB];
+      const T *fp = Fst + p * P + q0;
+#pragma unroll
+      for (int v = 0; v < FNV; ++v) {
+        if constexpr (FVB == 16 && ES == 4) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
+        } else if constexpr (FVB == 16 && ES == 8) {
+          const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
+          f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
+        } else {
+#pragma unroll
+          for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RS; ++r)
+#pragma unroll
+        for (int j = 0; j < QB; ++j) acc[r][j] = (p == 0) ? x[r][0] * f[j] : fma(x[r][p], f[j], acc[r][j]);
+    }
+#pragma unroll
+    for (int r = 0; r < RS; ++r) {
+      unsigned char *o = buf + wb[r] + (uint32_t)q0 * strideQ;
+#pragma unroll
+      for (int j = 0; j < QB; ++j) *reinterpret_cast<T *>(o + (uint32_t)j * strideQ) = acc[r][j];
+    }
+  }
+}
+
+template <typename T, int P, int RS, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) kron_fused_warp_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                  const __grid_constant__ CUtensorMap tm_out,
+                                                                  const FusedArgs a) {
+  constexpr int ES = sizeof(T);
+  constexpr int SLICE_BYTES = P * ES;
+  constexpr int VB = SLICE_BYTES < 16 ? SLICE_BYTES : 16;
+  constexpr int NV = SLICE_BYTES / VB;
+  constexpr int LINE = 128 / ES;
+  constexpr int GE = 32 * RS * P;  // elements of one warp's share of the tile
+
+  // [stages x tile][2 x output tile][factors][mbarriers], tiles 1024-aligned
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char *obase = base + (size_t)a.stages * a.stage_bytes;
+  T *Fs = reinterpret_cast<T *>(obase + (size_t)a.nout * a.stage_bytes);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(Fs) +
+                                                ((a.nf * P * P * ES + 15) & ~15));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int i = tid; i < a.nf * P * P; i += NT) {
+    const int st = i / (P * P), e = i - st * (P * P);
+    Fs[i] = reinterpret_cast<const T *>(a.F[st])[e];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+    prefetch_tmap(&tm_out);
+  }
+
+  const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
+  // warp phase: lane's slices lane + 32r of the warp's group
+  constexpr bool PRE = RS * P <= 16;
+  uint32_t rd0[RS][NV], rdg[RS][NV], wo[PRE ? RS : 1][PRE ? P : 1], wbase[RS], gx[RS];
+  const uint32_t strideCP = CP * ES;
+  const bool gm_on = C * ES >= 128;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const uint32_t el = (uint32_t)warp * GE + (uint32_t)(lane + 32 * r) * P;
+    const uint32_t gg = el / C, s = (el - gg * C) / P;
+    gx[r] = gm_on ? gmix(gg) << 4 : 0u;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      rd0[r][v] = swz128(el * ES + v * VB);
+      rdg[r][v] = swz_m(el * ES + v * VB, gx[r]);
+    }
+    wbase[r] = (gg * C + s) * ES;
+    if constexpr (PRE) {
+#pragma unroll
+      for (int q = 0; q < P; ++q) wo[r][q] = swz_m((gg * C + q * CP + s) * ES, gx[r]);
+    }
+  }
+  // last step: chunk-fastest slice order
+  uint32_t rl[RS][NV], wl[RS];
+  const bool chain = a.nf >= 2;
+#pragma unroll
+  for (int r = 0; r < RS; ++r) {
+    const uint32_t idx = (uint32_t)tid + (uint32_t)r * NT;
+    const uint32_t g = idx % R, rest = idx / R, s = rest % CP, row = rest / CP;
+    const uint32_t gg = row * R + g;
+    const uint32_t gxl = gm_on ? gmix(gg) << 4 : 0u;
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const uint32_t b = (gg * C + s * P) * ES + v * VB;
+      rl[r][v] = chain ? swz_m(b, gxl) : swz128(b);
+    }
+    wl[r] = (row * (uint32_t)a.tileK + s * R + g) * ES;
+  }
+  const uint32_t strideQ = (uint32_t)a.Sl * ES;
+  const bool noguard[RS] = {};
+  __syncthreads();
+
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * a.stage_bytes;
+    mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
+    const int line0 = cb * (a.tileK / LINE);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb * a.tileM);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+
+  for (int it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) break;
+    const int st = it % a.stages;
+    mbar_wait(&bars[st], (uint32_t)((it / a.stages) & 1));
+    unsigned char *buf = base + (size_t)st * a.stage_bytes;
+    unsigned char *ob = obase + (size_t)(a.nout == 2 ? (it & 1) : 0) * a.stage_bytes;
+    T x[RS][P];
+    if (chain) {
+      // a5: steps 0 .. nf-2 stay inside the warp (in place, chunk-swizzled)
+      load_slices<T, P, RS, NV, VB, false>(buf, rd0, noguard, x);
+      for (int step = 0; step < a.nf - 1; ++step) {
+        if (step > 0) load_slices<T, P, RS, NV, VB, false>(buf, rdg, noguard, x);
+        __syncwarp();
+        multiply_store_swz<T, P, RS, PRE>(buf, Fs + step * P * P, x, wo, wbase, gx, strideCP);
+        __syncwarp();
+      }
+    }
+    __syncthreads();  // warp-phase results visible; output buffer (it&1) released by the store of it-2
+    load_slices<T, P, RS, NV, VB, false>(buf, rl, noguard, x);
+    multiply_store_lin<T, P, RS>(ob, Fs + (a.nf - 1) * P * P, x, wl, strideQ);  // a6 source layout u*R + g
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+      tma_store_4d(&tm_out, ob, cb * a.R, 0, 0, rb * a.tileM);
+      bulk_commit();
+      issue_load(it + a.stages);  // this tile's stage is fully consumed
+      if (a.nout == 2)
+        bulk_wait_read<1>();  // the other output buffer is free for the next tile
+      else
+        bulk_wait_read<0>();  // the single output buffer is free for the next tile
+    }
+  }
+  if (tid == 0) bulk_wait<0>();
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
-    // dtype, P, NT, RS
-    {KRON_F32, 2, 256, 8},  {KRON_F32, 4, 256, 4},  {KRON_F32, 8, 128, 4},
-    {KRON_F32, 16, 256, 2}, {KRON_F32, 32, 128, 2}, {KRON_F64, 2, 256, 4},
-    {KRON_F64, 4, 256, 2},  {KRON_F64, 8, 256, 1},  {KRON_F64, 16, 128, 2},
-    {KRON_F64, 32, 128, 1},
+    // dtype, P, NT, RS, warp-chain
+    // v2 (warp-local chain): ids 0..9
+    {KRON_F32, 2, 256, 8, 1},  {KRON_F32, 4, 256, 4, 1},  {KRON_F32, 8, 256, 2, 1},
+    {KRON_F32, 16, 256, 2, 1}, {KRON_F32, 32, 256, 1, 1}, {KRON_F64, 2, 256, 4, 1},
+    {KRON_F64, 4, 256, 2, 1},  {KRON_F64, 8, 256, 1, 1},  {KRON_F64, 16, 256, 1, 1},
+    {KRON_F64, 32, 128, 1, 1},
+    // v1 (CTA-wide in-place chain, any chunk size): ids 10..19
+    {KRON_F32, 2, 256, 8, 0},  {KRON_F32, 4, 256, 4, 0},  {KRON_F32, 8, 128, 4, 0},
+    {KRON_F32, 16, 256, 2, 0}, {KRON_F32, 32, 128, 2, 0}, {KRON_F64, 2, 256, 4, 0},
+    {KRON_F64, 4, 256, 2, 0},  {KRON_F64, 8, 256, 1, 0},  {KRON_F64, 16, 128, 2, 0},
+    {KRON_F64, 32, 128, 1, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -253,16 +496,26 @@ using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs)
 
 KernelFn instance_kernel(int i) {
   switch (i) {
-    case 0: return kron_fused_kernel<float, 2, 8, 256>;
-    case 1: return kron_fused_kernel<float, 4, 4, 256>;
-    case 2: return kron_fused_kernel<float, 8, 4, 128>;
-    case 3: return kron_fused_kernel<float, 16, 2, 256>;
-    case 4: return kron_fused_kernel<float, 32, 2, 128>;
-    case 5: return kron_fused_kernel<double, 2, 4, 256>;
-    case 6: return kron_fused_kernel<double, 4, 2, 256>;
-    case 7: return kron_fused_kernel<double, 8, 1, 256>;
-    case 8: return kron_fused_kernel<double, 16, 2, 128>;
-    case 9: return kron_fused_kernel<double, 32, 1, 128>;
+    case 0: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
+    case 1: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
+    case 2: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
+    case 3: return kron_fused_warp_kernel<float, 16, 2, 256, 2>;
+    case 4: return kron_fused_warp_kernel<float, 32, 1, 256, 2>;
+    case 5: return kron_fused_warp_kernel<double, 2, 4, 256, 2>;
+    case 6: return kron_fused_warp_kernel<double, 4, 2, 256, 2>;
+    case 7: return kron_fused_warp_kernel<double, 8, 1, 256, 2>;
+    case 8: return kron_fused_warp_kernel<double, 16, 1, 256, 2>;
+    case 9: return kron_fused_warp_kernel<double, 32, 1, 128, 2>;
+    case 10: return kron_fused_kernel<float, 2, 8, 256>;
+    case 11: return kron_fused_kernel<float, 4, 4, 256>;
+    case 12: return kron_fused_kernel<float, 8, 4, 128>;
+    case 13: return kron_fused_kernel<float, 16, 2, 256>;
+    case 14: return kron_fused_kernel<float, 32, 2, 128>;
+    case 15: return kron_fused_kernel<double, 2, 4, 256>;
+    case 16: return kron_fused_kernel<double, 4, 2, 256>;
+    case 17: return kron_fused_kernel<double, 8, 1, 256>;
+    case 18: return kron_fused_kernel<double, 16, 2, 128>;
+    case 19: return kron_fused_kernel<double, 32, 1, 128>;
   }
   return nullptr;
 }
@@ -302,9 +555,9 @@ bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const u
 
 int fused_instance_count() { return kNumInstances; }
 const FusedInstance &fused_instance(int i) { return kInstances[i]; }
-int fused_find(int dtype, int P) {
+int fused_find(int dtype, int P, int warp) {
   for (int i = 0; i < kNumInstances; ++i)
-    if (kInstances[i].dtype == dtype && kInstances[i].P == P) return i;
+    if (kInstances[i].dtype == dtype && kInstances[i].P == P && kInstances[i].warp == warp) return i;
   return -1;
 }
 
@@ -323,6 +576,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.R = pp.R;
   a.Sl = (int)(pp.tileK / pp.P);
   a.nslices = pp.tileM * a.Sl;
+  a.C = (int)pp.C;
   a.tiles_k = (int)((WC + pp.R - 1) / pp.R);
   const int64_t tiles_m = (M + pp.tileM - 1) / pp.tileM;
   a.ntiles = tiles_m * a.tiles_k;
@@ -348,8 +602,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     if (!encode_tmap(&tout, dtype, 4, out, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
   }
 
-  const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes + (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) +
-                      8 * (size_t)a.stages;
+  a.nout = pp.nout;
+  const size_t smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
+                      (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
   KernelFn k = instance_kernel(pp.variant);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;

@@ -27,6 +27,7 @@ struct PassPlan {
   int64_t tileK = 0;
   int variant = -1;  // fused: kernel instance id; gemm: instance id
   int stages = 2;
+  int nout = 0;  // output staging buffers (warp-chain fused kernel)
   int src = BUF_X, dst = BUF_Y;
 };
 
@@ -50,11 +51,12 @@ struct FusedInstance {
   int P;
   int NT;     // threads per CTA
   int RS;     // slices per thread
+  int warp;   // 1: warp-local chain kernel (needs 32*RS*P % chunk == 0), 0: CTA-wide in-place chain
   int64_t elems() const { return (int64_t)NT * RS * P; }
 };
 int fused_instance_count();
 const FusedInstance &fused_instance(int i);
-int fused_find(int dtype, int P);  // instance id or -1
+int fused_find(int dtype, int P, int warp);  // instance id or -1
 
 // ---- launchers (device code lives in the .cu files).  Return cudaError_t as int.
 int launch_generic(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F,
