@@ -241,7 +241,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     if (plan->passes[i].W_out > max_interior) max_interior = plan->passes[i].W_out;
   const bool y_alt = max_interior <= plan->W[0];
   plan->nws = np <= 1 ? 0 : (y_alt || np == 2 ? 1 : 2);
-  plan->ws_elems = np <= 1 ? 0 : M * max_interior;
+  plan->ws_elems = np <= 1 ? 0 : (M * max_interior + 63) / 64 * 64;  // keep the second buffer 256B-aligned
   for (int i = np - 1, k = 0; i >= 0; --i, ++k) {
     int dst;
     if (k == 0) dst = BUF_Y;

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <vector>
 
+#include <cuda.h>
+
 #include "../../include/kron.h"
 
 namespace kron {
@@ -66,7 +68,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 
-// tensor-map encoder (driver entry point fetched through the runtime)
+// tensor-map encoder (driver entry point fetched through the runtime); fused.cu
 bool tmap_available();
+bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims, const uint64_t *strides,
+                 const uint32_t *box, bool swizzle128);
 
 }  // namespace kron
