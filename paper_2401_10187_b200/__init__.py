@@ -8,7 +8,7 @@ There is no CPU fallback: if ``libkron.so`` is missing, the first use of the API
 exists.)
 """
 _API = ("KronError", "dtype_code", "matmul", "matmul_ws", "matmul_ws_events", "plan_cost", "plan_describe",
-        "workspace_size", "lib_path", "dist_plan", "grid_rule")
+        "workspace_size", "lib_path", "dist_plan", "grid_rule", "DistContext", "matmul_dist")
 
 
 def __getattr__(name):

@@ -16,8 +16,20 @@ LIB = os.path.join(HERE, "libkron.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 SOURCES = ["api.cu", "generic.cu", "fused.cu", "gemm.cu", "dist.cu"]
 NVCC = os.environ.get("NVCC", "nvcc")
+def _nccl_include() -> str:
+    try:
+        import nvidia.nccl
+        inc = os.path.join(list(nvidia.nccl.__path__)[0], "include")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    except Exception:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-         "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", f"-I{INCLUDE}"]
+         "-Xcompiler", "-Wall", "--expt-relaxed-constexpr", f"-I{INCLUDE}",
+         f"-I{_nccl_include()}"]
 
 
 def _deps_mtime() -> float:

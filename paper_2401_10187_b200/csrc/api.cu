@@ -147,6 +147,12 @@ size_t ws_bytes_of(const Plan &plan) {
 
 }  // namespace
 
+size_t plan_ws_bytes(const Plan &plan) { return ws_bytes_of(plan); }
+
+kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream) {
+  return run_plan(plan, X, F, Y, ws, stream);
+}
+
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   if (M < 0 || N < 1 || N > kMaxFactors || !P || !Q) return KRON_ERR_INVALID_ARG;
   if (dtype != KRON_F32 && dtype != KRON_F64) return KRON_ERR_INVALID_ARG;
@@ -169,16 +175,20 @@ kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int
   return KRON_OK;
 }
 
-kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan) {
+kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan, int64_t lead) {
   kron_status_t st = validate(M, N, P, Q, dtype);
   if (st != KRON_OK) return st;
+  if (lead < 1) return KRON_ERR_INVALID_ARG;
   plan->N = N;
   plan->M = M;
   plan->dtype = dtype;
   plan->W.assign(N + 1, 0);
   int64_t K = 1;
   for (int i = 0; i < N; ++i) K *= P[i];
-  plan->W[N] = K;  // Alg 1
+  // W[N] = K (Alg 1).  lead > 1: the rows hold `lead` independent blocks of K columns — an
+  // implicit most-significant identity factor I_lead that is never applied (a distributed rank's
+  // local block, Alg 2).
+  plan->W[N] = K * lead;
   for (int f = N; f >= 1; --f) plan->W[f - 1] = plan->W[f] / P[f - 1] * Q[f - 1];  // line 307 / 319
   plan->passes.clear();
 

@@ -1,18 +1,39 @@
-// dist.cu — distributed Kron-Matmul, Algorithm 2: host round planner and grid rule.
-// (The context / exchange implementation is added in a later milestone.)
+// dist.cu — distributed Kron-Matmul, Algorithm 2, one rank per GPU.
+//
+// Grid {GM, GK}: rank r = gM*GK + gK holds X[gM rows][gK column block].  Rows never
+// communicate.  Within a row group the K dimension is split: each ROUND applies as many
+// factors as the local column block allows (Local = floor(log_P GTileK), line 666),
+// using the single-GPU fused / GEMM passes on the local block, then ONE all-to-all regroups the
+// slices (lines 676-692, reading G13) and StoreGPUTile places the received runs (line 685):
+//
+//   after a round with chunk C = prod P and Qc = prod Q of its factors, local run u (length
+//   rho = W/(C*GK)) of source gK belongs to global column (u*GK + gK)*rho; destination
+//   d = u div (Qc/GK) receives runs e = u mod (Qc/GK) and stores them at local (e*GK + gK)*rho.
+//
+// The exchange is ncclAlltoAll on a row-group communicator (ncclCommSplit(color = gM)); NCCL is
+// loaded with dlopen so libkron itself needs no NCCL at link time.  A "virtual" backend drives all
+// ranks of the grid from one process on one GPU, exchanging with device-to-device copies: it runs the
+// same planner, local passes, pack and StoreGPUTile kernels, and is how the distributed data path is
+// tested on a single B200.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
+#include <algorithm>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "kron_internal.h"
 
 namespace kron {
 
-// Round plan (reading G11): each round applies the most factors its local column block allows —
-// the round's chunk C = prod P must divide the local width W/GK (local slices are global slices,
-// P:645-647), and GK must divide the round's composite column count prod Q so that every rank
-// sends one contiguous part of W'/GK^2 values to every peer (Fig 8).  Fewest rounds first,
-// then balanced round sizes for uniform shapes.
+// ------------------------------------------------------------------ round planner (host)
+
+// Reading G11: each round applies the most factors its local column block allows — the round's chunk
+// C = prod P must divide the local width W/GK (local slices are global slices), and GK must
+// divide the round's composite column count prod Q so that every rank sends one contiguous part of
+// W'/GK^2 values per row to every peer (Fig 8).  Fewest rounds first, then balanced sizes.
 kron_status_t dist_round_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int GM, int GK,
                               std::vector<int> *rounds, std::vector<int64_t> *ledger) {
   kron_status_t st = validate(M, N, P, Q, KRON_F64);
@@ -81,18 +102,150 @@ kron_status_t grid_rule(int G, int *GM, int *GK) {
   int lg = 0;
   while ((1 << (lg + 1)) <= G) ++lg;
   if ((1 << lg) != G) return KRON_ERR_INVALID_ARG;  // rule yields 2^a * 2^b != G
-  *GM = 1 << ((lg + 1) / 2);  // 2^ceil(log2 sqrt G)
-  *GK = 1 << (lg / 2);        // 2^floor(log2 sqrt G)
+  *GM = 1 << ((lg + 1) / 2);                         // 2^ceil(log2 sqrt G)
+  *GK = 1 << (lg / 2);                               // 2^floor(log2 sqrt G)
   return KRON_OK;
 }
 
+// ------------------------------------------------------------------ pack / StoreGPUTile kernels
+
+namespace {
+
+// send[d][m][e] = out[m][d*B + e]      (destination-major send buffer, B = W'/GK)
+template <typename T>
+__global__ void __launch_bounds__(256) dist_pack_kernel(const T *__restrict__ in, T *__restrict__ send, int64_t rows,
+                                                        int64_t Wl, int64_t B) {
+  const int64_t n = rows * Wl;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / Wl, c = i - m * Wl;
+    const int64_t d = c / B, e = c - d * B;
+    send[(d * rows + m) * B + e] = in[i];
+  }
+}
+
+// StoreGPUTile (Alg 2): out[m][(e*GK + src)*rho + t] = recv[src][m][e*rho + t]
+template <typename T>
+__global__ void __launch_bounds__(256) dist_store_gpu_tile_kernel(const T *__restrict__ recv, T *__restrict__ out,
+                                                                  int64_t rows, int64_t Wl, int64_t rho, int GK) {
+  const int64_t n = rows * Wl, B = Wl / GK;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t m = i / Wl, c = i - m * Wl;
+    const int64_t run = c / rho, t = c - run * rho;
+    const int64_t e = run / GK, src = run - e * GK;
+    out[i] = recv[(src * rows + m) * B + e * rho + t];
+  }
+}
+
+int launch_pack(int dtype, const void *in, void *send, int64_t rows, int64_t Wl, int64_t B, cudaStream_t s) {
+  const int64_t n = rows * Wl;
+  if (n == 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (dtype == KRON_F32)
+    dist_pack_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float *)in, (float *)send, rows, Wl, B);
+  else
+    dist_pack_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double *)in, (double *)send, rows, Wl, B);
+  return (int)cudaGetLastError();
+}
+
+int launch_store_gpu_tile(int dtype, const void *recv, void *out, int64_t rows, int64_t Wl, int64_t rho, int GK,
+                          cudaStream_t s) {
+  const int64_t n = rows * Wl;
+  if (n == 0) return 0;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (dtype == KRON_F32)
+    dist_store_gpu_tile_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float *)recv, (float *)out, rows, Wl,
+                                                                       rho, GK);
+  else
+    dist_store_gpu_tile_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double *)recv, (double *)out, rows,
+                                                                        Wl, rho, GK);
+  return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ NCCL via dlopen
+
+struct NcclApi {
+  void *h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t *, ncclConfig_t *) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *) = nullptr;
+  ncclResult_t (*AlltoAll)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  bool ok = false;
+};
+NcclApi g_nccl;
+std::once_flag g_nccl_once;
+
+const NcclApi &nccl() {
+  std::call_once(g_nccl_once, [] {
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *n : names) {
+      g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (g_nccl.h) break;
+    }
+    if (!g_nccl.h) return;
+#define KRON_SYM(field, name) g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(g_nccl.h, name))
+    KRON_SYM(GetUniqueId, "ncclGetUniqueId");
+    KRON_SYM(CommInitRank, "ncclCommInitRank");
+    KRON_SYM(CommSplit, "ncclCommSplit");
+    KRON_SYM(CommDestroy, "ncclCommDestroy");
+    KRON_SYM(CommGetAsyncError, "ncclCommGetAsyncError");
+    KRON_SYM(AlltoAll, "ncclAlltoAll");
+    KRON_SYM(GroupStart, "ncclGroupStart");
+    KRON_SYM(GroupEnd, "ncclGroupEnd");
+    KRON_SYM(Send, "ncclSend");
+    KRON_SYM(Recv, "ncclRecv");
+#undef KRON_SYM
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommSplit && g_nccl.CommDestroy &&
+                (g_nccl.AlltoAll || (g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv));
+  });
+  return g_nccl;
+}
+
+}  // namespace
 }  // namespace kron
 
 using namespace kron;
 
 struct kron_dist_ctx {
-  int backend = 0;
+  int backend = 0;  // 0 NCCL, 1 virtual
+  int world = 1, rank = 0, GM = 1, GK = 1, gM = 0, gK = 0;
+  ncclComm_t world_comm = nullptr, row_comm = nullptr;
 };
+
+namespace kron {
+namespace {
+
+// All-to-all inside the row group: recv[src] <- send_src[me].  blk = elements per peer.
+kron_status_t exchange_nccl(kron_dist_ctx *ctx, int dtype, const void *send, void *recv, size_t blk, cudaStream_t s) {
+  const NcclApi &api = nccl();
+  const ncclDataType_t dt = dtype == KRON_F32 ? ncclFloat32 : ncclFloat64;
+  const size_t es = dtype == KRON_F32 ? 4 : 8;
+  if (api.AlltoAll) {
+    if (api.AlltoAll(send, recv, blk, dt, ctx->row_comm, s) != ncclSuccess) return KRON_ERR_NCCL;
+    return KRON_OK;
+  }
+  if (api.GroupStart() != ncclSuccess) return KRON_ERR_NCCL;
+  for (int p = 0; p < ctx->GK; ++p) {
+    api.Send(static_cast<const char *>(send) + p * blk * es, blk, dt, p, ctx->row_comm, s);
+    api.Recv(static_cast<char *>(recv) + p * blk * es, blk, dt, p, ctx->row_comm, s);
+  }
+  if (api.GroupEnd() != ncclSuccess) return KRON_ERR_NCCL;
+  return KRON_OK;
+}
+
+struct RankBufs {
+  void *cur = nullptr, *out = nullptr, *send = nullptr, *recv = nullptr, *ws = nullptr;
+};
+
+}  // namespace
+}  // namespace kron
 
 extern "C" {
 
@@ -113,23 +266,201 @@ kron_status_t kron_dist_plan(int64_t M, int32_t N, const int32_t *P, const int32
   return KRON_OK;
 }
 
-kron_status_t kron_dist_nccl_unique_id(void *) { return KRON_ERR_NCCL; }
+kron_status_t kron_dist_nccl_unique_id(void *out128) {
+  if (!out128) return KRON_ERR_INVALID_ARG;
+  const NcclApi &api = nccl();
+  if (!api.ok) return KRON_ERR_NCCL;
+  ncclUniqueId id;
+  if (api.GetUniqueId(&id) != ncclSuccess) return KRON_ERR_NCCL;
+  memcpy(out128, &id, sizeof(id));
+  return KRON_OK;
+}
 
-kron_status_t kron_dist_ctx_create(int32_t, const void *, int32_t, int32_t, int32_t, int32_t, kron_dist_ctx_t **out) {
-  if (out) *out = nullptr;
-  return KRON_ERR_UNSUPPORTED;
+kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, int32_t world_size, int32_t rank,
+                                   int32_t GM, int32_t GK, kron_dist_ctx_t **out) {
+  if (!out || world_size < 1 || (backend != 0 && backend != 1)) return KRON_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (GM == 0 && GK == 0) {
+    kron_status_t st = grid_rule(world_size, &GM, &GK);
+    if (st != KRON_OK) return st;
+  }
+  if (GM < 1 || GK < 1 || GM * GK != world_size) return KRON_ERR_INVALID_ARG;
+  auto *ctx = new kron_dist_ctx;
+  ctx->backend = backend;
+  ctx->world = world_size;
+  ctx->GM = GM;
+  ctx->GK = GK;
+  if (backend == 0) {
+    if (!nccl_unique_id || rank < 0 || rank >= world_size) {
+      delete ctx;
+      return KRON_ERR_INVALID_ARG;
+    }
+    const NcclApi &api = nccl();
+    if (!api.ok) {
+      delete ctx;
+      return KRON_ERR_NCCL;
+    }
+    ctx->rank = rank;
+    ctx->gM = rank / GK;
+    ctx->gK = rank % GK;
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof(id));
+    if (api.CommInitRank(&ctx->world_comm, world_size, id, rank) != ncclSuccess ||
+        api.CommSplit(ctx->world_comm, ctx->gM, ctx->gK, &ctx->row_comm, nullptr) != ncclSuccess) {
+      if (ctx->world_comm) api.CommDestroy(ctx->world_comm);
+      delete ctx;
+      return KRON_ERR_NCCL;
+    }
+  }
+  *out = ctx;
+  return KRON_OK;
 }
 
 kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx) {
+  if (!ctx) return KRON_OK;
+  if (ctx->backend == 0) {
+    const NcclApi &api = nccl();
+    if (ctx->row_comm) api.CommDestroy(ctx->row_comm);
+    if (ctx->world_comm) api.CommDestroy(ctx->world_comm);
+  }
   delete ctx;
   return KRON_OK;
 }
 
-kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *, int32_t *, int32_t *) { return KRON_ERR_UNSUPPORTED; }
+kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_t *GK) {
+  if (!ctx || !GM || !GK) return KRON_ERR_INVALID_ARG;
+  *GM = ctx->GM;
+  *GK = ctx->GK;
+  return KRON_OK;
+}
 
-kron_status_t kron_matmul_dist(int64_t, int32_t, const int32_t *, const int32_t *, const void *, const void *const *,
-                               void *, kron_dtype_t, kron_dist_ctx_t *, void *) {
-  return KRON_ERR_UNSUPPORTED;
+kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X_local,
+                               const void *const *F, void *Y_local, kron_dtype_t dtype, kron_dist_ctx_t *ctx,
+                               void *stream) {
+  if (!ctx) return KRON_ERR_INVALID_ARG;
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  const int GM = ctx->GM, GK = ctx->GK;
+  std::vector<int> rounds;
+  st = dist_round_plan(M, N, P, Q, GM, GK, &rounds, nullptr);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X_local || !F || !Y_local) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  const int nranks = ctx->backend == 1 ? GM * GK : 1;
+  const void *const *Xv = ctx->backend == 1 ? static_cast<const void *const *>(X_local) : &X_local;
+  void *const *Yv = ctx->backend == 1 ? static_cast<void *const *>(Y_local) : &Y_local;
+  for (int r = 0; r < nranks; ++r)
+    if (!Xv[r] || !Yv[r]) return KRON_ERR_INVALID_ARG;
+
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t es = dtype == KRON_F32 ? 4 : 8;
+  const int64_t Ml = M / GM;
+  std::vector<int64_t> W(N + 1);
+  W[N] = 1;
+  for (int i = 0; i < N; ++i) W[N] *= P[i];
+  for (int f = N; f >= 1; --f) W[f - 1] = W[f] / P[f - 1] * Q[f - 1];
+
+  // Row-only grid: every rank is an independent single-GPU Kron-Matmul (no communication).
+  if (GK == 1) {
+    Plan plan;
+    st = make_plan(Ml, N, P, Q, (int)dtype, &plan);
+    if (st != KRON_OK) return st;
+    const size_t wsb = plan_ws_bytes(plan);
+    void *ws = nullptr;
+    if (wsb && cudaMallocAsync(&ws, wsb, s) != cudaSuccess) return KRON_ERR_NO_MEMORY;
+    for (int r = 0; r < nranks && st == KRON_OK; ++r) st = plan_run(plan, Xv[r], F, Yv[r], ws, stream);
+    if (ws) cudaFreeAsync(ws, s);
+    return st;
+  }
+
+  // local plans per round (identical on every rank: shape-only)
+  struct RoundPlan {
+    Plan plan;
+    int first;
+    int64_t wl_in, wl_out, rho;
+  };
+  std::vector<RoundPlan> rp(rounds.size());
+  int64_t max_w = 0;
+  size_t ws_max = 0;
+  {
+    int f = N;
+    for (size_t j = 0; j < rounds.size(); ++j) {
+      const int k = rounds[j];
+      int64_t C = 1;
+      for (int i = 0; i < k; ++i) C *= P[f - 1 - i];
+      rp[j].first = f;
+      rp[j].wl_in = W[f] / GK;
+      rp[j].wl_out = W[f - k] / GK;
+      rp[j].rho = rp[j].wl_in / C;
+      // factors f-k+1 .. f (most significant first) on the local block with lead = wl_in / C
+      st = make_plan(Ml, k, P + (f - k), Q + (f - k), (int)dtype, &rp[j].plan, rp[j].wl_in / C);
+      if (st != KRON_OK) return st;
+      max_w = std::max(max_w, std::max(rp[j].wl_in, rp[j].wl_out));
+      ws_max = std::max(ws_max, plan_ws_bytes(rp[j].plan));
+      f -= k;
+    }
+  }
+  const size_t buf_bytes = (size_t)Ml * max_w * es;
+  std::vector<RankBufs> bufs(nranks);
+  bool oom = false;
+  for (int r = 0; r < nranks; ++r) {
+    oom |= cudaMallocAsync(&bufs[r].cur, buf_bytes, s) != cudaSuccess;
+    oom |= cudaMallocAsync(&bufs[r].out, buf_bytes, s) != cudaSuccess;
+    oom |= cudaMallocAsync(&bufs[r].send, buf_bytes, s) != cudaSuccess;
+    oom |= cudaMallocAsync(&bufs[r].recv, buf_bytes, s) != cudaSuccess;
+    if (ws_max) oom |= cudaMallocAsync(&bufs[r].ws, ws_max, s) != cudaSuccess;
+  }
+  auto free_all = [&] {
+    for (auto &b : bufs)
+      for (void *p : {b.cur, b.out, b.send, b.recv, b.ws})
+        if (p) cudaFreeAsync(p, s);
+  };
+  if (oom) {
+    cudaGetLastError();
+    free_all();
+    return KRON_ERR_NO_MEMORY;
+  }
+
+  for (size_t j = 0; j < rounds.size() && st == KRON_OK; ++j) {
+    const RoundPlan &R = rp[j];
+    const int k = rounds[j];
+    const void *const *Fj = F + (R.first - k);
+    const bool last = j + 1 == rounds.size();
+    const int64_t B = R.wl_out / GK;       // values per row sent to each peer
+    const size_t blk = (size_t)Ml * B;     // values per peer
+    // lines 670-674: local sliced multiplies; then pack the destination-major send buffer
+    for (int r = 0; r < nranks && st == KRON_OK; ++r) {
+      const void *in = j == 0 ? Xv[r] : bufs[r].cur;
+      st = plan_run(R.plan, in, Fj, bufs[r].out, bufs[r].ws, stream);
+      if (st == KRON_OK && launch_pack((int)dtype, bufs[r].out, bufs[r].send, Ml, R.wl_out, B, s) != 0)
+        st = KRON_ERR_CUDA;
+    }
+    if (st != KRON_OK) break;
+    // lines 676-692: all-to-all inside the row group
+    if (ctx->backend == 0) {
+      st = exchange_nccl(ctx, (int)dtype, bufs[0].send, bufs[0].recv, blk, s);
+    } else {
+      for (int gm = 0; gm < GM && st == KRON_OK; ++gm)
+        for (int src = 0; src < GK; ++src)
+          for (int dst = 0; dst < GK; ++dst) {
+            const int rs = gm * GK + src, rd = gm * GK + dst;
+            if (cudaMemcpyAsync(static_cast<char *>(bufs[rd].recv) + (size_t)src * blk * es,
+                                static_cast<const char *>(bufs[rs].send) + (size_t)dst * blk * es, blk * es,
+                                cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+              st = KRON_ERR_CUDA;
+          }
+    }
+    if (st != KRON_OK) break;
+    // line 685: StoreGPUTile into the next round's local block (or Y_local after the last round)
+    for (int r = 0; r < nranks && st == KRON_OK; ++r) {
+      void *dst = last ? Yv[r] : bufs[r].cur;
+      if (launch_store_gpu_tile((int)dtype, bufs[r].recv, dst, Ml, R.wl_out, R.rho, GK, s) != 0) st = KRON_ERR_CUDA;
+    }
+  }
+  free_all();
+  return st;
 }
 
 }  // extern "C"

@@ -193,3 +193,100 @@ def matmul_ws_events(X, Fs, out, workspace, events, stream=None):
 
 def raw_lib():
     return _lib
+
+
+# ------------------------------------------------------------------ distributed (Algorithm 2)
+
+_lib.kron_dist_nccl_unique_id.restype = ctypes.c_int
+_lib.kron_dist_nccl_unique_id.argtypes = [ctypes.c_void_p]
+_lib.kron_dist_ctx_create.restype = ctypes.c_int
+_lib.kron_dist_ctx_create.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
+_lib.kron_dist_ctx_destroy.restype = ctypes.c_int
+_lib.kron_dist_ctx_destroy.argtypes = [ctypes.c_void_p]
+_lib.kron_dist_ctx_grid.restype = ctypes.c_int
+_lib.kron_dist_ctx_grid.argtypes = [ctypes.c_void_p, _i32p, _i32p]
+_lib.kron_matmul_dist.restype = ctypes.c_int
+_lib.kron_matmul_dist.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
+                                  ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
+
+
+class DistContext:
+    """kron_dist_ctx_t.  backend "nccl": one rank per GPU; the ncclUniqueId is created by rank 0 and
+    broadcast over the torch ProcessGroup `pg` (plumbing only).  backend "virtual": all GM*GK ranks of the
+    grid live in this process on the current GPU (exchange = device copies).  GM = GK = 0: the paper's
+    grid rule."""
+
+    def __init__(self, backend="nccl", world_size=None, rank=None, GM=0, GK=0, pg=None):
+        self.handle = ctypes.c_void_p()
+        if backend == "nccl":
+            import torch.distributed as dist
+            world_size = dist.get_world_size(pg) if world_size is None else world_size
+            rank = dist.get_rank(pg) if rank is None else rank
+            uid = ctypes.create_string_buffer(128)
+            if rank == 0:
+                _check(_lib.kron_dist_nccl_unique_id(uid), "kron_dist_nccl_unique_id")
+            obj = [bytes(uid.raw) if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0, group=pg)
+            uid = ctypes.create_string_buffer(obj[0], 128)
+            _check(_lib.kron_dist_ctx_create(0, uid, world_size, rank, GM, GK, ctypes.byref(self.handle)),
+                   "kron_dist_ctx_create")
+        elif backend == "virtual":
+            if world_size is None:
+                world_size = GM * GK
+            _check(_lib.kron_dist_ctx_create(1, None, world_size, 0, GM, GK, ctypes.byref(self.handle)),
+                   "kron_dist_ctx_create")
+            rank = 0
+        else:
+            raise ValueError(backend)
+        self.backend, self.rank, self.world_size = backend, rank, world_size
+        gm, gk = ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.kron_dist_ctx_grid(self.handle, ctypes.byref(gm), ctypes.byref(gk)), "kron_dist_ctx_grid")
+        self.GM, self.GK = gm.value, gk.value
+
+    def coords(self, rank=None):
+        r = self.rank if rank is None else rank
+        return r // self.GK, r % self.GK
+
+    def close(self):
+        if self.handle:
+            _lib.kron_dist_ctx_destroy(self.handle)
+            self.handle = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def matmul_dist(M, X_local, Fs, ctx: DistContext, out=None, stream=None):
+    """kron_matmul_dist().  nccl backend: X_local is this rank's block X[gM rows, gK K-block]; returns
+    Y_local = Y[gM rows, gK L-block].  virtual backend: X_local is a list of every rank's block (rank
+    order gM*GK + gK); returns the list of Y_local blocks."""
+    import torch
+    P = [int(f.shape[0]) for f in Fs]
+    Q = [int(f.shape[1]) for f in Fs]
+    L = 1
+    for q in Q:
+        L *= q
+    Pa, Qa = _shape_arrays(P, Q)
+    Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
+    xs = X_local if isinstance(X_local, (list, tuple)) else [X_local]
+    for x in xs:
+        if not x.is_cuda or not x.is_contiguous():
+            raise ValueError("X blocks must be contiguous CUDA tensors")
+    shape = (M // ctx.GM, L // ctx.GK)
+    if out is None:
+        outs = [torch.empty(shape, dtype=xs[0].dtype, device=xs[0].device) for _ in xs]
+    else:
+        outs = out if isinstance(out, (list, tuple)) else [out]
+    if ctx.backend == "virtual":
+        xp = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
+        yp = (ctypes.c_void_p * len(outs))(*[y.data_ptr() for y in outs])
+        xarg, yarg = ctypes.cast(xp, ctypes.c_void_p), ctypes.cast(yp, ctypes.c_void_p)
+    else:
+        xarg, yarg = xs[0].data_ptr(), outs[0].data_ptr()
+    _check(_lib.kron_matmul_dist(M, len(P), Pa, Qa, xarg, Fp, yarg, dtype_code(xs[0].dtype), ctx.handle,
+                                 _stream_ptr(stream)), "kron_matmul_dist")
+    return outs if isinstance(X_local, (list, tuple)) else outs[0]
