@@ -208,6 +208,79 @@ def run_reference(args, cfg_name):
     return 0
 
 
+def run_dist(args, ws, rank, local, dev, barrier):
+    """Strong scaling of one configuration over a {GM,GK} grid with kron_matmul_dist (NCCL)."""
+    import torch
+    import synth
+    from paper_2401_10187_b200 import kron
+    cfg, M, P, Q, dtn = CONFIGS[args.config]
+    dt = np.float32 if dtn == "float32" else np.float64
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    es = 4 if dt == np.float32 else 8
+    seed = synth.SEED_BASE + cfg
+    K, L = int(np.prod(P)), int(np.prod(Q))
+    GM, GK = (0, 0) if args.grid is None else (int(v) for v in args.grid.lower().split("x"))
+    if ws == 1:
+        GM, GK = 1, 1
+    if ws > 1:
+        ctx = kron.DistContext("nccl", GM=GM, GK=GK)
+    else:
+        ctx = kron.DistContext("virtual", GM=1, GK=1)
+    gm, gk = ctx.coords(rank)
+    Ml, Kl = M // ctx.GM, K // ctx.GK
+    stream = torch.cuda.current_stream()
+    X = torch.empty((Ml, Kl), dtype=tdt, device=dev)
+    synth.fill_device(X.data_ptr(), Ml, Kl, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=gm * Ml,
+                      c0=gk * Kl, ld=K)
+    Fs = [torch.from_numpy(f).to(dev) for f in synth.factors(P, Q, seed, "urand", dt)]
+    Y = torch.empty((Ml, L // ctx.GK), dtype=tdt, device=dev)
+    xs, ys = (X, Y) if ctx.backend == "nccl" else ([X], [Y])
+    for _ in range(args.warmup):
+        kron.matmul_dist(M, xs, Fs, ctx, out=ys)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        t0.record(stream)
+        for _ in range(args.steps):
+            kron.matmul_dist(M, xs, Fs, ctx, out=ys)
+        t1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = t0.elapsed_time(t1)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    rounds, ledger = kron.dist_plan(M, P, Q, ctx.GM, ctx.GK)
+    fl_step = flops_of(M, P, Q)
+    value = fl_step * args.steps / (ms / 1e3) / 1e9
+    hbm_peak, hbm_src = measured_peaks()
+    alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
+    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt)
+    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12)) / ws
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+            "data": "synthetic (seeded counter-based U[0,1), each rank generates its own block in HBM)",
+            "config": {"workload": args.config, "M": M, "P": P, "Q": Q, "grid": [ctx.GM, ctx.GK],
+                       "rounds": rounds, "exchanged_values_per_step": int(sum(ledger)),
+                       "parallelism": f"Algorithm 2 grid {ctx.GM}x{ctx.GK} (rows x K), NCCL all-to-all",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "step_roofline": {"t_roof_ms_per_gpu": round(t_roof * 1e3, 4),
+                              "frac": round(t_roof / (ms / args.steps / 1e3), 4)},
+            "gpu_launches": None, "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -218,6 +291,10 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dist", action="store_true",
+                    help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
+                         "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
+    ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -241,6 +318,9 @@ def main():
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
+
+    if args.dist:
+        return run_dist(args, ws, rank, local, dev, barrier)
 
     cfg, M, P, Q, dtn = CONFIGS[args.config]
     dt = np.float32 if dtn == "float32" else np.float64
