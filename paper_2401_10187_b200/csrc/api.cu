@@ -53,16 +53,26 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   if (tileM > 1 && lines > 256) return false;
   if (C > 256 && (C % 256 || C / 256 > 256)) return false;
-  if (inst.warp && ((int64_t)32 * inst.RS * p) % C) return false;  // warp share = whole chunks
+  if (inst.warp && ((int64_t)32 * inst.rsw * p) % C) return false;  // warp share = whole chunks
+  if (inst.warp == 2) {
+    if (k > 3) return false;                                   // one warp group per factor
+    if (R % inst.rsw || (k >= 2 && C < (int64_t)inst.rsw * p)) return false;  // 16-byte chunk/slice vectors
+    if (tileM * R / inst.rsw * (C / p) > 4 * inst.NT) return false;        // <= 4 last-step slots per thread
+  }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp) {
+  if (inst.warp == 2) {
+    nout = 2;
+    stages = (int)((200 * 1024 - 2 * stage) / stage);  // deep ring: one CTA per SM
+    if (stages > 8) stages = 8;
+    if (stages < k + 1) return false;
+  } else if (inst.warp == 1) {
     stages = 2;
     nout = stage <= 16 * 1024 ? 2 : 1;  // keep >= 2 CTAs per SM
   } else {
     stages = stage <= 32 * 1024 ? 3 : 2;
   }
-  const int64_t smem = 1024 + (stages + nout) * stage + (int64_t)k * p * p * es + 16 + 8 * stages;
+  const int64_t smem = 1024 + (stages + nout) * stage + (int64_t)k * p * p * es + 16 + 32 * stages;
   if (smem > 227 * 1024) return false;
   pp->kind = KIND_FUSED;
   pp->nf = k;
@@ -197,6 +207,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
   while (f >= 1) {
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
+    const int inst_p = (p == q) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q) ? fused_find(dtype, p, 1) : -1;
     const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;
     if (inst_c >= 0) {
@@ -204,6 +215,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_p >= 0 && fused_geometry(fused_instance(inst_p), k, W, Mp, pp)) return inst_p;
         if (inst_w >= 0 && fused_geometry(fused_instance(inst_w), k, W, Mp, pp)) return inst_w;
         if (fused_geometry(fused_instance(inst_c), k, W, Mp, pp)) return inst_c;
         return -1;

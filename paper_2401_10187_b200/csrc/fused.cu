@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 
 #include <mutex>
+#include <type_traits>
 
 #include "kron_internal.h"
 #include "ptx.cuh"
@@ -86,24 +87,48 @@ __device__ __forceinline__ void load_slices(const unsigned char *buf, const uint
   }
 }
 
-// One sliced multiply of the register-resident slices with the factor Fst (shared, [p][q]) and the
-// in-place store of out[row][q*Sl + s].  SWZ: 0 linear layout (last step, TMA-store source),
-// 1 swizzled with the q-stride a multiple of 1024 B (swizzle commutes with +q*stride), 2 general.
-template <typename T, int P, int RS, int SWZ>
-__device__ __forceinline__ void multiply_store(unsigned char *buf, const T *Fst, const T (&x)[RS][P],
-                                               const uint32_t (&wb)[RS], const bool (&act)[RS], uint32_t strideQ) {
+// acc[r][j] = sum_p x[r][p] * F[p][q0 + j] with F row-major (P x P) in shared memory, read as
+// warp-uniform broadcasts.  fp32 uses Blackwell's paired FMA (FFMA2: two FMAs per instruction, x as a
+// broadcast operand): profiles/r01_microbench_ffma2.jsonl measured 73 TFLOP/s for FFMA2 against
+// 60 TFLOP/s for scalar FFMA in this loop shape, with half the issue slots.
+template <typename T, int P, int RS, int QB>
+__device__ __forceinline__ void mac_block(const T *Fst, int q0, const T (&x)[RS][P], T (&acc)[RS][QB]) {
   constexpr int ES = sizeof(T);
-  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;  // factor columns per broadcast group
-  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
-  constexpr int FNV = QB * ES / FVB;
-  constexpr int FEPV = FVB / ES;
+  if constexpr (ES == 4 && QB % 2 == 0) {
+    float2 acc2[RS][QB / 2];
 #pragma unroll
-  for (int q0 = 0; q0 < P; q0 += QB) {
-    T acc[RS][QB];
+    for (int p = 0; p < P; ++p) {
+      float2 f2[QB / 2];
+      const float *fp = reinterpret_cast<const float *>(Fst) + p * P + q0;
+      if constexpr (QB % 4 == 0) {
+#pragma unroll
+        for (int v = 0; v < QB / 4; ++v) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(fp + 4 * v);
+          f2[2 * v] = make_float2(t4.x, t4.y);
+          f2[2 * v + 1] = make_float2(t4.z, t4.w);
+        }
+      } else {
+#pragma unroll
+        for (int v = 0; v < QB / 2; ++v) f2[v] = *reinterpret_cast<const float2 *>(fp + 2 * v);
+      }
+#pragma unroll
+      for (int r = 0; r < RS; ++r) {
+        const float2 xx = make_float2(x[r][p], x[r][p]);
+#pragma unroll
+        for (int j = 0; j < QB / 2; ++j) acc2[r][j] = p == 0 ? __fmul2_rn(xx, f2[j]) : __ffma2_rn(xx, f2[j], acc2[r][j]);
+      }
+    }
 #pragma unroll
     for (int r = 0; r < RS; ++r)
 #pragma unroll
-      for (int j = 0; j < QB; ++j) acc[r][j] = T(0);
+      for (int j = 0; j < QB / 2; ++j) {
+        acc[r][2 * j] = acc2[r][j].x;
+        acc[r][2 * j + 1] = acc2[r][j].y;
+      }
+  } else {
+    constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
+    constexpr int FNV = QB * ES / FVB;
+    constexpr int FEPV = FVB / ES;
 #pragma unroll
     for (int p = 0; p < P; ++p) {
       T f[QB];
@@ -124,8 +149,26 @@ __device__ __forceinline__ void multiply_store(unsigned char *buf, const T *Fst,
 #pragma unroll
       for (int r = 0; r < RS; ++r)
 #pragma unroll
-        for (int j = 0; j < QB; ++j) acc[r][j] = fma(x[r][p], f[j], acc[r][j]);
+        for (int j = 0; j < QB; ++j) acc[r][j] = p == 0 ? x[r][0] * f[j] : fma(x[r][p], f[j], acc[r][j]);
     }
+  }
+}
+
+// One sliced multiply of the register-resident slices with the factor Fst (shared, [p][q]) and the
+// in-place store of out[row][q*Sl + s].  SWZ: 0 linear layout (last step, TMA-store source),
+// 1 swizzled with the q-stride a multiple of 1024 B (swizzle commutes with +q*stride), 2 general.
+template <typename T, int P, int RS, int SWZ>
+__device__ __forceinline__ void multiply_store(unsigned char *buf, const T *Fst, const T (&x)[RS][P],
+                                               const uint32_t (&wb)[RS], const bool (&act)[RS], uint32_t strideQ) {
+  constexpr int ES = sizeof(T);
+  constexpr int QB = (P * ES >= 32) ? 32 / ES : P;  // factor columns per broadcast group
+  constexpr int FVB = (QB * ES) < 16 ? QB * ES : 16;
+  constexpr int FNV = QB * ES / FVB;
+  constexpr int FEPV = FVB / ES;
+#pragma unroll
+  for (int q0 = 0; q0 < P; q0 += QB) {
+    T acc[RS][QB];
+    mac_block<T, P, RS, QB>(Fst, q0, x, acc);
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
       if (!act[r]) continue;
@@ -270,28 +313,7 @@ __device__ __forceinline__ void multiply_store_swz(unsigned char *buf, const T *
 #pragma unroll
   for (int q0 = 0; q0 < P; q0 += QB) {
     T acc[RS][QB];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      T f[QB];
-      const T *fp = Fst + p * P + q0;
-#pragma unroll
-      for (int v = 0; v < FNV; ++v) {
-        if constexpr (FVB == 16 && ES == 4) {
-          const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
-          f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
-        } else if constexpr (FVB == 16 && ES == 8) {
-          const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
-          f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
-        } else {
-#pragma unroll
-          for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RS; ++r)
-#pragma unroll
-        for (int j = 0; j < QB; ++j) acc[r][j] = (p == 0) ? x[r][0] * f[j] : fma(x[r][p], f[j], acc[r][j]);
-    }
+    mac_block<T, P, RS, QB>(Fst, q0, x, acc);
 #pragma unroll
     for (int r = 0; r < RS; ++r)
 #pragma unroll
@@ -320,28 +342,7 @@ __device__ __forceinline__ void multiply_store_lin(unsigned char *buf, const T *
 #pragma unroll
   for (int q0 = 0; q0 < P; q0 += QB) {
     T acc[RS][QB];
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      T f[QB];
-      const T *fp = Fst + p * P + q0;
-#pragma unroll
-      for (int v = 0; v < FNV; ++v) {
-        if constexpr (FVB == 16 && ES == 4) {
-          const float4 t4 = *reinterpret_cast<const float4 *>(fp + v * FEPV);
-          f[v * FEPV + 0] = t4.x; f[v * FEPV + 1] = t4.y; f[v * FEPV + 2] = t4.z; f[v * FEPV + 3] = t4.w;
-        } else if constexpr (FVB == 16 && ES == 8) {
-          const double2 t2 = *reinterpret_cast<const double2 *>(fp + v * FEPV);
-          f[v * FEPV + 0] = t2.x; f[v * FEPV + 1] = t2.y;
-        } else {
-#pragma unroll
-          for (int e = 0; e < FEPV; ++e) f[v * FEPV + e] = fp[v * FEPV + e];
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < RS; ++r)
-#pragma unroll
-        for (int j = 0; j < QB; ++j) acc[r][j] = (p == 0) ? x[r][0] * f[j] : fma(x[r][p], f[j], acc[r][j]);
-    }
+    mac_block<T, P, RS, QB>(Fst, q0, x, acc);
 #pragma unroll
     for (int r = 0; r < RS; ++r) {
       unsigned char *o = buf + wb[r] + (uint32_t)q0 * strideQ;
@@ -475,20 +476,329 @@ __global__ void __launch_bounds__(NT, MINB) kron_fused_warp_kernel(const __grid_
   if (tid == 0) bulk_wait<0>();
 }
 
+// acc[q] = sum_p x[p] * F[p][q] with the factor held in registers (fp32: as FFMA2 pairs).
+template <typename T, int P>
+struct RegFactor {
+  static constexpr bool kPair = sizeof(T) == 4 && P % 2 == 0;
+  typename std::conditional<kPair, float2, T>::type f[P][kPair ? P / 2 : P];
+  __device__ __forceinline__ void load(const T *F) {
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      if constexpr (kPair) {
+#pragma unroll
+        for (int j = 0; j < P / 2; ++j) f[p][j] = make_float2(F[p * P + 2 * j], F[p * P + 2 * j + 1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < P; ++q) f[p][q] = F[p * P + q];
+      }
+    }
+  }
+  __device__ __forceinline__ void mac(const T (&x)[P], T (&acc)[P]) const {
+    if constexpr (kPair) {
+      float2 a2[P / 2];
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const float2 xx = make_float2(x[p], x[p]);
+#pragma unroll
+        for (int j = 0; j < P / 2; ++j) a2[j] = p == 0 ? __fmul2_rn(xx, f[p][j]) : __ffma2_rn(xx, f[p][j], a2[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < P / 2; ++j) {
+        acc[2 * j] = a2[j].x;
+        acc[2 * j + 1] = a2[j].y;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < P; ++q) acc[q] = x[0] * f[0][q];
+#pragma unroll
+      for (int p = 1; p < P; ++p)
+#pragma unroll
+        for (int q = 0; q < P; ++q) acc[q] = fma(x[p], f[p][q], acc[q]);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ factor-pipelined chain (v3)
+//
+// Small factors (P*P values fit in registers: fp32 P <= 8, fp64 P <= 4).  The CTA is split into one
+// producer warp (TMA loads) and one group of NWG warps PER FACTOR of the fused group (<= 3).  Group g
+// keeps its factor F_{f-g} in registers for the whole kernel and applies it to every tile, in place on
+// the stage buffer; tiles flow through the groups like a pipeline (mbarriers done[g][stage]), so the
+// factor is never re-read from shared memory — only the data moves through shared memory (one read
+// and one write per factor and element).
+//   middle groups: a lane owns VS consecutive slices of one chunk (VS*P contiguous elements), so the
+//     outputs of a column q are VS consecutive values: one 16-byte store per column;
+//   last group: a thread owns VS consecutive chunks for one slice index (chunk-fastest order), so its
+//     outputs are VS consecutive values of the final u*R + g layout: one 16-byte store per column into
+//     the double-buffered output tile, which one TMA tensor store sends to HBM.
+// Bank conflicts: the TMA 128B swizzle plus an XOR of the 16-byte granule with bitrev3(chunk) (chosen
+// with a bank-conflict model over the three access patterns).
+// linear maps over GF(2)^3 (3x3 bit matrices) picked by exhaustive search with the bank model
+template <int P, int ES>
+__device__ __forceinline__ uint32_t pipe_gx(uint32_t chunk) {
+  const uint32_t g0 = chunk & 1u, g1 = (chunk >> 1) & 1u, g2 = (chunk >> 2) & 1u;
+  if constexpr (P == 8 && ES == 4) return (g2 | (g1 << 1) | ((g0 ^ g1) << 2)) << 4;
+  else return (g2 | (g1 << 1) | ((g0 ^ g2) << 2)) << 4;
+}
+
+template <typename T, int N>
+struct VecIO;
+template <>
+struct VecIO<float, 2> {
+  __device__ __forceinline__ static void st(unsigned char *p, const float (&v)[2]) {
+    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+  }
+};
+template <>
+struct VecIO<float, 4> {
+  __device__ __forceinline__ static void st(unsigned char *p, const float (&v)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <>
+struct VecIO<double, 2> {
+  __device__ __forceinline__ static void st(unsigned char *p, const double (&v)[2]) {
+    *reinterpret_cast<double2 *>(p) = make_double2(v[0], v[1]);
+  }
+};
+
+template <typename T, int P, int NWG, int VS, int G>
+__device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
+                                           unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
+                                           int wg, int lane, int tid);
+
+template <typename T, int P, int NWG, int VS>
+__global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
+    kron_fused_pipe_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
+                           const FusedArgs a) {
+  constexpr int ES = sizeof(T);               // VS: consecutive slices (middle) / chunks (last) per thread
+  constexpr int LINE = 128 / ES;
+  constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
+  constexpr int EPV = 16 / ES > P ? P : 16 / ES;
+  constexpr int VB = EPV * ES;
+  constexpr int MAXNF = 3;
+  static_assert(P * ES >= 8, "slice >= 8 bytes");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char *obase = base + (size_t)a.stages * a.stage_bytes;
+  uint64_t *full = reinterpret_cast<uint64_t *>(obase + 2 * (size_t)a.stage_bytes);
+  uint64_t *empty = full + a.stages;
+  uint64_t *done = empty + a.stages;  // [MAXNF-1][stages]
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  const int nf = a.nf;
+
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      for (int g = 0; g < MAXNF - 1; ++g) mbar_init(&done[g * a.stages + s], NWG);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+    prefetch_tmap(&tm_out);
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer: TMA loads into the stage ring
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int64_t tile = blockIdx.x, it = 0; tile < a.ntiles; tile += gridDim.x, ++it) {
+        if (it >= a.stages) mbar_wait(&empty[st], ph ^ 1u);
+        const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+        unsigned char *dst = base + (size_t)st * a.stage_bytes;
+        mbar_arrive_expect_tx(&full[st], a.tile_bytes);
+        const int line0 = cb * (a.tileK / LINE);
+        for (int b = 0; b < a.nbox; ++b)
+          tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines,
+                      rb * a.tileM);
+        if (++st == a.stages) {
+          st = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+  const int g = (warp - 1) / NWG, wg = (warp - 1) % NWG;
+  if (g >= nf) return;
+  // one code path per group index so that the factor pointer (kernel parameter) and hence every
+  // factor value is provably warp-uniform: the compiler keeps F in uniform registers
+  if (g == 0) pipe_group<T, P, NWG, VS, 0>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
+  else if (g == 1) pipe_group<T, P, NWG, VS, 1>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
+  else pipe_group<T, P, NWG, VS, 2>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
+}
+
+template <typename T, int P, int NWG, int VS, int G>
+__device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
+                                           unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
+                                           int wg, int lane, int tid) {
+  constexpr int ES = sizeof(T);
+  constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
+  constexpr int EPV = 16 / ES > P ? P : 16 / ES;
+  constexpr int VB = EPV * ES;
+  const int g = G, nf = a.nf;
+  // this group's factor F_{first-g} lives in (uniform) registers for the whole kernel
+  RegFactor<T, P> Fr;
+  Fr.load(reinterpret_cast<const T *>(a.F[G]));
+  const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
+  const uint32_t tile_elems = (uint32_t)a.tileM * (uint32_t)a.tileK;
+  const bool gx_on = C * ES >= 128;  // the granule XOR must be constant over each 128-byte line
+
+  if (g < nf - 1) {
+    // ---------------- middle group: lane owns VS consecutive slices; warp regions of 32*VS*P elements
+    constexpr uint32_t GE = 32u * VS * P;
+    const uint32_t el = (uint32_t)lane * VS * P;            // first element of my slices in the region
+    const uint32_t cl = el / C, s0 = (el - cl * C) / P;     // chunk within the region, first slice
+    const uint32_t nreg = tile_elems / GE;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+      mbar_wait(g == 0 ? &full[st] : &done[(g - 1) * a.stages + st], ph);
+      unsigned char *buf = base + (size_t)st * a.stage_bytes;
+#pragma unroll 1
+      for (uint32_t grp = (uint32_t)wg; grp < nreg; grp += NWG) {
+        unsigned char *gb = buf + grp * (GE * ES);
+        const uint32_t chunk = grp * (GE / C) + cl;
+        const uint32_t gx = gx_on ? pipe_gx<P, ES>(chunk) : 0u;
+        const uint32_t gxr = g == 0 ? 0u : gx;  // step 0 reads the plain TMA layout
+        T x[VS][P];
+#pragma unroll
+        for (int r = 0; r < VS; ++r)
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const uint32_t off = swz128((el + r * P) * ES + v * VB) ^ gxr;
+            if constexpr (ES == 4 && EPV == 4) {
+              const float4 t4 = *reinterpret_cast<const float4 *>(gb + off);
+              x[r][4 * v] = t4.x; x[r][4 * v + 1] = t4.y; x[r][4 * v + 2] = t4.z; x[r][4 * v + 3] = t4.w;
+            } else if constexpr (ES == 4 && EPV == 2) {
+              const float2 t2 = *reinterpret_cast<const float2 *>(gb + off);
+              x[r][0] = t2.x; x[r][1] = t2.y;
+            } else {
+              const double2 t2 = *reinterpret_cast<const double2 *>(gb + off);
+              x[r][2 * v] = t2.x; x[r][2 * v + 1] = t2.y;
+            }
+          }
+        __syncwarp();
+        T acc[VS][P];
+#pragma unroll
+        for (int r = 0; r < VS; ++r) Fr.mac(x[r], acc[r]);
+        const uint32_t ob = (cl * C + s0) * ES;  // chunk-local output index q*CP + s0
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          T v[VS];
+#pragma unroll
+          for (int r = 0; r < VS; ++r) v[r] = acc[r][q];
+          VecIO<T, VS>::st(gb + (swz128(ob + (uint32_t)q * CP * ES) ^ gx), v);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mbar_arrive(&done[g * a.stages + st]);
+      if (++st == a.stages) {
+        st = 0;
+        ph ^= 1u;
+      }
+    }
+    return;
+  }
+
+  // ---------------- last group: thread owns VS consecutive chunks for one slice (chunk-fastest)
+  const int lt = tid - 32 * (1 + g * NWG);
+  constexpr int LT = NWG * 32;
+  const uint32_t nq = R / VS;                       // chunk groups per tile row
+  const uint32_t slots = (uint32_t)a.tileM * nq * CP;
+  const uint32_t strideQ = (uint32_t)a.Sl * ES;
+  const bool chained = nf >= 2;
+  // per-thread slot geometry (identical for every tile): first chunk and output offset
+  constexpr int MAXSL = 4;
+  const int nsl = (int)((slots + LT - 1) / LT);
+  uint32_t sl_chunk[MAXSL], sl_s[MAXSL], sl_out[MAXSL];
+#pragma unroll
+  for (int k = 0; k < MAXSL; ++k) {
+    const uint32_t slot = (uint32_t)lt + (uint32_t)k * LT;
+    const uint32_t j = slot % nq, rest = slot / nq, s = rest % CP, row = rest / CP;
+    sl_chunk[k] = row * R + j * VS;
+    sl_s[k] = s;
+    sl_out[k] = (row * (uint32_t)a.tileK + s * R + j * VS) * ES;
+  }
+  int st = 0;
+  uint32_t ph = 0;
+  for (int64_t tile = blockIdx.x, it = 0; tile < a.ntiles; tile += gridDim.x, ++it) {
+    mbar_wait(nf == 1 ? &full[st] : &done[(nf - 2) * a.stages + st], ph);
+    named_bar_sync(1, LT);  // the store that last read this output buffer has finished reading it
+    const unsigned char *buf = base + (size_t)st * a.stage_bytes;
+    unsigned char *obuf = obase + (size_t)(it & 1) * a.stage_bytes;
+#pragma unroll
+    for (int k = 0; k < MAXSL; ++k) {
+      if (k >= nsl) break;
+      const uint32_t s = sl_s[k];
+      T acc[VS][P];
+#pragma unroll
+      for (int i = 0; i < VS; ++i) {
+        const uint32_t chunk = sl_chunk[k] + i;
+        const uint32_t gx = (chained && gx_on) ? pipe_gx<P, ES>(chunk) : 0u;
+        T x[P];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+          const uint32_t off = swz128((chunk * C + s * P) * ES + v * VB) ^ gx;
+          if constexpr (ES == 4 && EPV == 4) {
+            const float4 t4 = *reinterpret_cast<const float4 *>(buf + off);
+            x[4 * v] = t4.x; x[4 * v + 1] = t4.y; x[4 * v + 2] = t4.z; x[4 * v + 3] = t4.w;
+          } else if constexpr (ES == 4 && EPV == 2) {
+            const float2 t2 = *reinterpret_cast<const float2 *>(buf + off);
+            x[0] = t2.x; x[1] = t2.y;
+          } else {
+            const double2 t2 = *reinterpret_cast<const double2 *>(buf + off);
+            x[2 * v] = t2.x; x[2 * v + 1] = t2.y;
+          }
+        }
+        Fr.mac(x, acc[i]);
+      }
+      unsigned char *o = obuf + sl_out[k];
+#pragma unroll
+      for (int q = 0; q < P; ++q) {
+        T v[VS];
+#pragma unroll
+        for (int i = 0; i < VS; ++i) v[i] = acc[i][q];
+        VecIO<T, VS>::st(o + (uint32_t)q * strideQ, v);
+      }
+    }
+    fence_proxy_async_smem();
+    named_bar_sync(2, LT);
+    if (lt == 0) {
+      mbar_arrive(&empty[st]);  // every group is done with this stage
+      const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+      tma_store_4d(tm_out, obuf, cb * a.R, 0, 0, rb * a.tileM);
+      bulk_commit();
+      bulk_wait_read<1>();
+    }
+    if (++st == a.stages) {
+      st = 0;
+      ph ^= 1u;
+    }
+  }
+  if (lt == 0) bulk_wait<0>();
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
-    // dtype, P, NT, RS, warp-chain
-    // v2 (warp-local chain): ids 0..9
-    {KRON_F32, 2, 256, 8, 1},  {KRON_F32, 4, 256, 4, 1},  {KRON_F32, 8, 256, 2, 1},
-    {KRON_F32, 16, 256, 2, 1}, {KRON_F32, 32, 256, 1, 1}, {KRON_F64, 2, 256, 4, 1},
-    {KRON_F64, 4, 256, 2, 1},  {KRON_F64, 8, 256, 1, 1},  {KRON_F64, 16, 256, 1, 1},
-    {KRON_F64, 32, 128, 1, 1},
-    // v1 (CTA-wide in-place chain, any chunk size): ids 10..19
-    {KRON_F32, 2, 256, 8, 0},  {KRON_F32, 4, 256, 4, 0},  {KRON_F32, 8, 128, 4, 0},
-    {KRON_F32, 16, 256, 2, 0}, {KRON_F32, 32, 128, 2, 0}, {KRON_F64, 2, 256, 4, 0},
-    {KRON_F64, 4, 256, 2, 0},  {KRON_F64, 8, 256, 1, 0},  {KRON_F64, 16, 128, 2, 0},
-    {KRON_F64, 32, 128, 1, 0},
+    // dtype, P, NT (threads doing the last step), RS (slices per thread, last step), kind, rsw
+    // v3 factor-pipelined (factors in registers): ids 0..4
+    {KRON_F32, 2, 128, 16, 2, 4}, {KRON_F32, 4, 128, 8, 2, 4}, {KRON_F32, 8, 128, 4, 2, 2},
+    {KRON_F64, 2, 128, 8, 2, 2},  {KRON_F64, 4, 128, 4, 2, 2},
+    // v2 (warp-local chain): ids 5..14
+    {KRON_F32, 2, 256, 8, 1, 8},  {KRON_F32, 4, 256, 4, 1, 4},  {KRON_F32, 8, 256, 2, 1, 2},
+    {KRON_F32, 16, 256, 2, 1, 2}, {KRON_F32, 32, 256, 1, 1, 1}, {KRON_F64, 2, 256, 4, 1, 4},
+    {KRON_F64, 4, 256, 2, 1, 2},  {KRON_F64, 8, 256, 1, 1, 1},  {KRON_F64, 16, 256, 1, 1, 1},
+    {KRON_F64, 32, 128, 1, 1, 1},
+    // v1 (CTA-wide in-place chain, any chunk size): ids 15..24
+    {KRON_F32, 2, 256, 8, 0, 0},  {KRON_F32, 4, 256, 4, 0, 0},  {KRON_F32, 8, 128, 4, 0, 0},
+    {KRON_F32, 16, 256, 2, 0, 0}, {KRON_F32, 32, 128, 2, 0, 0}, {KRON_F64, 2, 256, 4, 0, 0},
+    {KRON_F64, 4, 256, 2, 0, 0},  {KRON_F64, 8, 256, 1, 0, 0},  {KRON_F64, 16, 128, 2, 0, 0},
+    {KRON_F64, 32, 128, 1, 0, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -496,26 +806,31 @@ using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs)
 
 KernelFn instance_kernel(int i) {
   switch (i) {
-    case 0: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
-    case 1: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
-    case 2: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
-    case 3: return kron_fused_warp_kernel<float, 16, 2, 256, 2>;
-    case 4: return kron_fused_warp_kernel<float, 32, 1, 256, 2>;
-    case 5: return kron_fused_warp_kernel<double, 2, 4, 256, 2>;
-    case 6: return kron_fused_warp_kernel<double, 4, 2, 256, 2>;
-    case 7: return kron_fused_warp_kernel<double, 8, 1, 256, 2>;
-    case 8: return kron_fused_warp_kernel<double, 16, 1, 256, 2>;
-    case 9: return kron_fused_warp_kernel<double, 32, 1, 128, 2>;
-    case 10: return kron_fused_kernel<float, 2, 8, 256>;
-    case 11: return kron_fused_kernel<float, 4, 4, 256>;
-    case 12: return kron_fused_kernel<float, 8, 4, 128>;
-    case 13: return kron_fused_kernel<float, 16, 2, 256>;
-    case 14: return kron_fused_kernel<float, 32, 2, 128>;
-    case 15: return kron_fused_kernel<double, 2, 4, 256>;
-    case 16: return kron_fused_kernel<double, 4, 2, 256>;
-    case 17: return kron_fused_kernel<double, 8, 1, 256>;
-    case 18: return kron_fused_kernel<double, 16, 2, 128>;
-    case 19: return kron_fused_kernel<double, 32, 1, 128>;
+    case 0: return kron_fused_pipe_kernel<float, 2, 4, 4>;
+    case 1: return kron_fused_pipe_kernel<float, 4, 4, 4>;
+    case 2: return kron_fused_pipe_kernel<float, 8, 4, 2>;
+    case 3: return kron_fused_pipe_kernel<double, 2, 4, 2>;
+    case 4: return kron_fused_pipe_kernel<double, 4, 4, 2>;
+    case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
+    case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
+    case 7: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
+    case 8: return kron_fused_warp_kernel<float, 16, 2, 256, 2>;
+    case 9: return kron_fused_warp_kernel<float, 32, 1, 256, 2>;
+    case 10: return kron_fused_warp_kernel<double, 2, 4, 256, 2>;
+    case 11: return kron_fused_warp_kernel<double, 4, 2, 256, 2>;
+    case 12: return kron_fused_warp_kernel<double, 8, 1, 256, 2>;
+    case 13: return kron_fused_warp_kernel<double, 16, 1, 256, 2>;
+    case 14: return kron_fused_warp_kernel<double, 32, 1, 128, 2>;
+    case 15: return kron_fused_kernel<float, 2, 8, 256>;
+    case 16: return kron_fused_kernel<float, 4, 4, 256>;
+    case 17: return kron_fused_kernel<float, 8, 4, 128>;
+    case 18: return kron_fused_kernel<float, 16, 2, 256>;
+    case 19: return kron_fused_kernel<float, 32, 2, 128>;
+    case 20: return kron_fused_kernel<double, 2, 4, 256>;
+    case 21: return kron_fused_kernel<double, 4, 2, 256>;
+    case 22: return kron_fused_kernel<double, 8, 1, 256>;
+    case 23: return kron_fused_kernel<double, 16, 2, 128>;
+    case 24: return kron_fused_kernel<double, 32, 1, 128>;
   }
   return nullptr;
 }
@@ -603,13 +918,20 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   }
 
   a.nout = pp.nout;
-  const size_t smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
-                      (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
+  size_t smem;
+  int threads = inst.NT;
+  if (inst.warp == 2) {
+    smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
+    threads = 32 * (1 + 3 * (inst.NT / 32));  // producer warp + one warp group per factor (max 3)
+  } else {
+    smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
+           (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
+  }
   KernelFn k = instance_kernel(pp.variant);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, inst.NT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
   if (e != cudaSuccess) return (int)e;
   if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
   int dev = 0, sms = 148;
@@ -617,7 +939,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > a.ntiles) grid = a.ntiles;
-  k<<<(unsigned)grid, inst.NT, smem, (cudaStream_t)stream>>>(tin, tout, a);
+  k<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a);
   return (int)cudaGetLastError();
 }
 

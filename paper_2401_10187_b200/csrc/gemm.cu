@@ -123,10 +123,24 @@ __global__ void __launch_bounds__(256, 1) kron_gemm_kernel(const __grid_constant
         T b[TN];
 #pragma unroll
         for (int j = 0; j < TN; ++j) b[j] = sb[(pp + e) * BN + tn + GN * j];
+        if constexpr (ES == 4) {
+          // FFMA2: two columns per instruction, a[i] broadcast
 #pragma unroll
-        for (int i = 0; i < TM; ++i)
+          for (int i = 0; i < TM; ++i) {
+            const float2 aa = make_float2(a[i][e], a[i][e]);
 #pragma unroll
-          for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i][e], b[j], acc[i][j]);
+            for (int j = 0; j < TN; j += 2) {
+              float2 c = __ffma2_rn(aa, make_float2(b[j], b[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+              acc[i][j] = c.x;
+              acc[i][j + 1] = c.y;
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j] = fma(a[i][e], b[j], acc[i][j]);
+        }
       }
     }
     __syncthreads();  // stage st fully read

@@ -57,7 +57,8 @@ struct FusedInstance {
   int P;
   int NT;     // threads per CTA
   int RS;     // slices per thread
-  int warp;   // 1: warp-local chain kernel (needs 32*RS*P % chunk == 0), 0: CTA-wide in-place chain
+  int warp;   // 2: factor-pipelined kernel, 1: warp-local chain kernel, 0: CTA-wide in-place chain
+  int rsw;    // slices per lane in the warp-owned (intermediate) steps; 32*rsw*P % chunk == 0 needed
   int64_t elems() const { return (int64_t)NT * RS * P; }
 };
 int fused_instance_count();
