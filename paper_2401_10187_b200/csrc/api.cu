@@ -54,6 +54,10 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   if (tileM > 1 && lines > 256) return false;
   if (C > 256 && (C % 256 || C / 256 > 256)) return false;
   if (inst.warp && ((int64_t)32 * inst.rsw * p) % C) return false;  // warp share = whole chunks
+  if (inst.warp == 3) {
+    // two-factor chunk GEMMs: exactly two factors, one tile row of whole chunk octets
+    if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
+  }
   if (inst.warp == 2) {
     if (k > 3) return false;                                   // one warp group per factor
     if (R % inst.rsw || (k >= 2 && C < (int64_t)inst.rsw * p)) return false;  // 16-byte chunk/slice vectors
@@ -61,7 +65,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 2) {
+  if (inst.warp == 3) {
+    stages = 3;
+  } else if (inst.warp == 2) {
     nout = 2;
     stages = (int)((200 * 1024 - 2 * stage) / stage);  // deep ring: one CTA per SM
     if (stages > 8) stages = 8;
@@ -207,6 +213,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
   while (f >= 1) {
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
+    const int inst_g = (p == q) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q) ? fused_find(dtype, p, 1) : -1;
     const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;
@@ -215,6 +222,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_g >= 0 && fused_geometry(fused_instance(inst_g), k, W, Mp, pp)) return inst_g;
         if (inst_p >= 0 && fused_geometry(fused_instance(inst_p), k, W, Mp, pp)) return inst_p;
         if (inst_w >= 0 && fused_geometry(fused_instance(inst_w), k, W, Mp, pp)) return inst_w;
         if (fused_geometry(fused_instance(inst_c), k, W, Mp, pp)) return inst_c;

@@ -42,6 +42,10 @@ struct FusedArgs {
   int nslices;    // tileM * Sl
   int C;          // chunk = P^nf
   int nout;       // output buffers (warp-chain kernel): 2 = double-buffered TMA-store source
+  void *Y;        // output matrix (kernels that store from registers)
+  int64_t WC;     // W / C  (output column stride of a composite column u)
+  int64_t Wout;   // output row width
+  int64_t M;      // rows
   int tiles_k;    // tiles along a row
   int64_t ntiles;
   int nbox;       // input TMA boxes per tile (along dim1)
@@ -782,6 +786,221 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   if (lt == 0) bulk_wait<0>();
 }
 
+// ------------------------------------------------------------------ two-factor GEMM chunks (v4)
+//
+// Two square factors of size P = 16 / 32 (configs C and E).  A chunk (C = P^2 elements) is a P x P
+// matrix X[s][p] (rows = slices), and the fused pair of sliced multiplies is the sandwich
+//     OUT[q2][q1] = sum_s F2[s][q2] * Z[s][q1],   Z = X . F1            (u = q2*P + q1)
+// i.e. two P x P x P matrix products per chunk, done with register-tiled FFMA2 (fp32) / DFMA (fp64):
+//   GEMM1 (warp-local): each lane computes an RM x RN tile of Z for one chunk, reading X rows and F1
+//     rows as 16-byte vectors, and writes Z back in place (row-major, chunk-swizzled);
+//   GEMM2 (CTA-wide, chunk-fastest): lane = (chunk of an octet, q2 group) so that for every output the
+//     8 lanes of a q2 group hold 8 consecutive chunks: their stores to u*(W/C) + g0 + g form full
+//     32-byte sectors (the direct-index store of P:325-329, issued from registers).
+// Loads of the tile use TMA (128B swizzle) through an mbarrier ring, as in the other fused kernels.
+template <typename T, int P, int RM, int RN, int NW, int MINB>
+__global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                        const FusedArgs a) {
+  constexpr int ES = sizeof(T);
+  constexpr int LINE = 128 / ES;
+  constexpr int C = P * P;
+  constexpr int VA = 16 / ES;                 // p-values per 16-byte X load
+  constexpr int L1 = (P / RM) * (P / RN);     // lane tiles per chunk
+  constexpr int CPG = 32 / L1;                // chunks per warp in GEMM1
+  static_assert(L1 <= 32 && 32 % L1 == 0, "GEMM1 lane tiling");
+  static_assert(P % (4 * RM) == 0, "GEMM2: 4 q2 groups per warp");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  T *Fs = reinterpret_cast<T *>(base + (size_t)a.stages * a.stage_bytes);  // [2][P][P]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(reinterpret_cast<unsigned char *>(Fs) + 2 * P * P * ES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  for (int i = tid; i < 2 * P * P; i += NW * 32) {
+    const int st = i / (P * P), e = i - st * (P * P);
+    Fs[i] = reinterpret_cast<const T *>(a.F[st])[e];
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  const T *F1 = Fs, *F2 = Fs + P * P;
+  const int nchunks = a.R;  // tileM == 1
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * a.stage_bytes;
+    mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
+    const int line0 = cb * (a.tileK / LINE);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+
+  // GEMM1 lane geometry
+  const int c1 = lane / L1, tau = lane % L1;
+  const int sg = tau % (P / RM), q1g = tau / (P / RM);
+  // GEMM2 lane geometry
+  const int gl = lane & 7, q2s = lane >> 3;
+  constexpr int U2_Q1 = P / RN, U2_Q2 = P / (4 * RM);
+  const int units2 = (nchunks / 8) * U2_Q1 * U2_Q2;
+  T *Y = reinterpret_cast<T *>(a.Y);
+
+  for (int it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) break;
+    const int st = it % a.stages;
+    mbar_wait(&bars[st], (uint32_t)((it / a.stages) & 1));
+    unsigned char *buf = base + (size_t)st * a.stage_bytes;
+
+    // ---------------- GEMM1: Z = X . F1 per chunk (warp-local, in place)
+    for (int cg = warp; cg * CPG < nchunks; cg += NW) {
+      const uint32_t gg = (uint32_t)(cg * CPG + c1);
+      const uint32_t cbase = gg * C * ES;
+      const uint32_t gx = pipe_gx<8, 4>(gg);
+      T acc[RM][RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+#pragma unroll 2
+      for (int p0 = 0; p0 < P; p0 += VA) {
+        T xa[RM][VA];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) {
+          const int s = sg + (P / RM) * i;
+          const unsigned char *src = buf + swz128(cbase + (uint32_t)(s * P + p0) * ES);
+          if constexpr (ES == 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(src);
+            xa[i][0] = v.x; xa[i][1] = v.y; xa[i][2] = v.z; xa[i][3] = v.w;
+          } else {
+            const double2 v = *reinterpret_cast<const double2 *>(src);
+            xa[i][0] = v.x; xa[i][1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < VA; ++e) {
+          T f[RN];
+          const T *fr = F1 + (p0 + e) * P + q1g * RN;
+#pragma unroll
+          for (int j = 0; j < RN; j += VA) {
+            if constexpr (ES == 4) {
+              const float4 v = *reinterpret_cast<const float4 *>(fr + j);
+              f[j] = v.x; f[j + 1] = v.y; f[j + 2] = v.z; f[j + 3] = v.w;
+            } else {
+              const double2 v = *reinterpret_cast<const double2 *>(fr + j);
+              f[j] = v.x; f[j + 1] = v.y;
+            }
+          }
+#pragma unroll
+          for (int i = 0; i < RM; ++i) {
+            if constexpr (ES == 4) {
+              const float2 xx = make_float2(xa[i][e], xa[i][e]);
+#pragma unroll
+              for (int j = 0; j < RN; j += 2) {
+                const float2 r2 = __ffma2_rn(xx, make_float2(f[j], f[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+                acc[i][j] = r2.x;
+                acc[i][j + 1] = r2.y;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < RN; ++j) acc[i][j] = fma(xa[i][e], f[j], acc[i][j]);
+            }
+          }
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < RM; ++i) {
+        const int s = sg + (P / RM) * i;
+#pragma unroll
+        for (int j = 0; j < RN; j += VA) {
+          unsigned char *dst = buf + (swz128(cbase + (uint32_t)(s * P + q1g * RN + j) * ES) ^ gx);
+          if constexpr (ES == 4)
+            *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+          else
+            *reinterpret_cast<double2 *>(dst) = make_double2(acc[i][j], acc[i][j + 1]);
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // ---------------- GEMM2: OUT = F2^T . Z, chunk-fastest lanes, stores from registers
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    for (int u2 = warp; u2 < units2; u2 += NW) {
+      const int oct = u2 / (U2_Q1 * U2_Q2), rest = u2 - oct * (U2_Q1 * U2_Q2);
+      const int q1b = rest % U2_Q1, q2b = rest / U2_Q1;
+      const uint32_t gg = (uint32_t)(oct * 8 + gl);
+      const uint32_t cbase = gg * C * ES;
+      const uint32_t gx = pipe_gx<8, 4>(gg);
+      const int q2base = (q2b * 4 + q2s) * RM, q1base = q1b * RN;
+      T acc[RM][RN];
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+#pragma unroll 4
+      for (int s = 0; s < P; ++s) {
+        T fv[RM], zv[RN];
+        const T *fr = F2 + s * P + q2base;
+#pragma unroll
+        for (int i = 0; i < RM; i += VA) {
+          if constexpr (ES == 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(fr + i);
+            fv[i] = v.x; fv[i + 1] = v.y; fv[i + 2] = v.z; fv[i + 3] = v.w;
+          } else {
+            const double2 v = *reinterpret_cast<const double2 *>(fr + i);
+            fv[i] = v.x; fv[i + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < RN; j += VA) {
+          const unsigned char *src = buf + (swz128(cbase + (uint32_t)(s * P + q1base + j) * ES) ^ gx);
+          if constexpr (ES == 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(src);
+            zv[j] = v.x; zv[j + 1] = v.y; zv[j + 2] = v.z; zv[j + 3] = v.w;
+          } else {
+            const double2 v = *reinterpret_cast<const double2 *>(src);
+            zv[j] = v.x; zv[j + 1] = v.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < RM; ++i) {
+          if constexpr (ES == 4) {
+            const float2 ff = make_float2(fv[i], fv[i]);
+#pragma unroll
+            for (int j = 0; j < RN; j += 2) {
+              const float2 r2 = __ffma2_rn(ff, make_float2(zv[j], zv[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+              acc[i][j] = r2.x;
+              acc[i][j + 1] = r2.y;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < RN; ++j) acc[i][j] = fma(fv[i], zv[j], acc[i][j]);
+          }
+        }
+      }
+      // direct-index store: u = q2*P + q1 -> Y[row][u*(W/C) + cb*R + g]
+      const int64_t gcol = (int64_t)cb * a.R + gg;
+      if (gcol < a.WC && rb < a.M) {
+        T *yrow = Y + (int64_t)rb * a.Wout + gcol;
+#pragma unroll
+        for (int i = 0; i < RM; ++i)
+#pragma unroll
+          for (int j = 0; j < RN; ++j) yrow[(int64_t)((q2base + i) * P + q1base + j) * a.WC] = acc[i][j];
+      }
+    }
+    __syncthreads();  // the stage is fully consumed
+    if (tid == 0) issue_load(it + a.stages);
+  }
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
@@ -789,6 +1008,7 @@ const FusedInstance kInstances[] = {
     // v3 factor-pipelined (factors in registers): ids 0..4
     {KRON_F32, 2, 128, 16, 2, 4}, {KRON_F32, 4, 128, 8, 2, 4}, {KRON_F32, 8, 128, 4, 2, 2},
     {KRON_F64, 2, 128, 8, 2, 2},  {KRON_F64, 4, 128, 4, 2, 2},
+    // v4 two-factor GEMM chunks (nf == 2 only): ids 25..26 appended at the end
     // v2 (warp-local chain): ids 5..14
     {KRON_F32, 2, 256, 8, 1, 8},  {KRON_F32, 4, 256, 4, 1, 4},  {KRON_F32, 8, 256, 2, 1, 2},
     {KRON_F32, 16, 256, 2, 1, 2}, {KRON_F32, 32, 256, 1, 1, 1}, {KRON_F64, 2, 256, 4, 1, 4},
@@ -799,10 +1019,21 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 16, 256, 2, 0, 0}, {KRON_F32, 32, 128, 2, 0, 0}, {KRON_F64, 2, 256, 4, 0, 0},
     {KRON_F64, 4, 256, 2, 0, 0},  {KRON_F64, 8, 256, 1, 0, 0},  {KRON_F64, 16, 128, 2, 0, 0},
     {KRON_F64, 32, 128, 1, 0, 0},
+    // v4: two-factor chunk GEMMs (tile = 256 * RS * P elements = 8192)
+    {KRON_F32, 16, 256, 2, 3, 0}, {KRON_F32, 32, 256, 1, 3, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs);
+using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
+
+Kernel4Fn instance_kernel4(int i) {
+  switch (i) {
+    case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
+    case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
+  }
+  return nullptr;
+}
 
 KernelFn instance_kernel(int i) {
   switch (i) {
@@ -918,14 +1149,36 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   }
 
   a.nout = pp.nout;
+  a.Y = out;
+  a.WC = WC;
+  a.Wout = Wout;
+  a.M = M;
   size_t smem;
   int threads = inst.NT;
-  if (inst.warp == 2) {
+  if (inst.warp == 3) {
+    smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
+  } else if (inst.warp == 2) {
     smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
     threads = 32 * (1 + 3 * (inst.NT / 32));  // producer warp + one warp group per factor (max 3)
   } else {
     smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
+  }
+  if (inst.warp == 3) {
+    Kernel4Fn k4 = instance_kernel4(pp.variant);
+    cudaError_t e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4, threads, smem);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t grid = (int64_t)sms * per_sm;
+    if (grid > a.ntiles) grid = a.ntiles;
+    k4<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, a);
+    return (int)cudaGetLastError();
   }
   KernelFn k = instance_kernel(pp.variant);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
