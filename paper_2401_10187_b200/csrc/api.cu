@@ -66,7 +66,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
   if (inst.warp == 3) {
-    stages = 3;
+    stages = stage <= 32 * 1024 ? 3 : 2;
   } else if (inst.warp == 2) {
     nout = 2;
     stages = (int)((200 * 1024 - 2 * stage) / stage);  // deep ring: one CTA per SM

@@ -1021,6 +1021,7 @@ const FusedInstance kInstances[] = {
     {KRON_F64, 32, 128, 1, 0, 0},
     // v4: two-factor chunk GEMMs (tile = 256 * RS * P elements = 8192)
     {KRON_F32, 16, 256, 2, 3, 0}, {KRON_F32, 32, 256, 1, 3, 0},
+    {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1031,6 +1032,8 @@ Kernel4Fn instance_kernel4(int i) {
   switch (i) {
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
+    case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 2>;
+    case 28: return kron_fused_gemm2_kernel<double, 32, 4, 8, 8, 1>;
   }
   return nullptr;
 }
