@@ -75,10 +75,9 @@ def main():
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for d in s:
         name = d["kernel"]
-        key = next((k for k in ("kron_fused_kernel", "kron_fused_warp_kernel", "kron_gemm_kernel",
-                                "sliced_generic_kernel") if k in name), None)
+        key = ("kron_fused_kernel" if "kron_fused" in name else "kron_gemm_kernel" if "kron_gemm" in name
+               else "sliced_generic_kernel" if "sliced_generic" in name else None)
         if key and "dram_bytes" in d:
-            key = "kron_fused_kernel" if key == "kron_fused_warp_kernel" else key
             traffic.setdefault(cfg, {})[key] = int(d["dram_bytes"])
     with open(tpath, "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
