@@ -163,6 +163,22 @@ size_t ws_bytes_of(const Plan &plan) {
 
 }  // namespace
 
+// kron_matmul() reserves its workspace with cudaMallocAsync on the caller's stream.  Keep freed blocks
+// in the device's default memory pool (release threshold = max) so repeated calls do not re-map GiBs
+// of workspace every time.
+void keep_pool_cached() {
+  static std::once_flag once[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+  std::call_once(once[dev], [dev] {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+}
+
 size_t plan_ws_bytes(const Plan &plan) { return ws_bytes_of(plan); }
 
 kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream) {
@@ -363,6 +379,7 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
   void *ws = nullptr;
   cudaStream_t s = (cudaStream_t)stream;
   if (need > 0) {
+    keep_pool_cached();
     if (cudaMallocAsync(&ws, need, s) != cudaSuccess) {
       cudaGetLastError();
       return KRON_ERR_NO_MEMORY;

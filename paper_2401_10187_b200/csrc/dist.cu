@@ -355,6 +355,7 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     if (!Xv[r] || !Yv[r]) return KRON_ERR_INVALID_ARG;
 
   cudaStream_t s = (cudaStream_t)stream;
+  keep_pool_cached();
   const size_t es = dtype == KRON_F32 ? 4 : 8;
   const int64_t Ml = M / GM;
   std::vector<int64_t> W(N + 1);

@@ -596,7 +596,7 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      for (int g = 0; g < MAXNF - 1; ++g) mbar_init(&done[g * a.stages + s], NWG);
+      for (int g = 0; g < MAXNF - 1; ++g) mbar_init(&done[g * a.stages + s], NWG * 32);
     }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
@@ -699,7 +699,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
         }
         __syncwarp();
       }
-      if (lane == 0) mbar_arrive(&done[g * a.stages + st]);
+      mbar_arrive(&done[g * a.stages + st]);  // every lane releases its own in-place writes
       if (++st == a.stages) {
         st = 0;
         ph ^= 1u;

@@ -47,6 +47,7 @@ struct Plan {
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
                         int64_t lead = 1);
 size_t plan_ws_bytes(const Plan &plan);
+void keep_pool_cached();  // default mem pool keeps freed blocks (stream-ordered workspaces)
 // Enqueue every pass of `plan` (F indexed like the plan's P/Q arrays); ws >= plan_ws_bytes bytes.
 kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream);
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype);

@@ -1,0 +1,48 @@
+#!/usr/bin/env python
+"""Small-shape runs of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck).
+
+    compute-sanitizer --tool racecheck python tools/sanitize.py
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2401_10187_b200 import kron  # noqa: E402
+
+CASES = [
+    (9, [8] * 6, np.float32),        # v3 factor pipeline (3,3)
+    (3, [32] * 2, np.float32),       # v4 chunk GEMMs (2)
+    (2, [16] * 3, np.float32),       # v4 (2) + v2 (1)
+    (2, [32] * 2, np.float64),       # v4 fp64
+    (5, [4] * 5, np.float64),        # v3 fp64 / v2
+    (3, [16] * 3, np.float64),       # v1/v2 fp64
+    (2, [64, 64], np.float64),       # gemm
+    (3, [3, 5], np.float32),         # generic
+]
+
+
+def main():
+    dev = torch.device("cuda:0")
+    for M, P, dt in CASES:
+        seed = synth.SEED_BASE + 77
+        X = synth.matrix(M, int(np.prod(P)), seed, 0, "urand", dt)
+        Fs = synth.factors(P, P, seed, "urand", dt)
+        Y = kron.matmul(torch.from_numpy(X).to(dev), [torch.from_numpy(f).to(dev) for f in Fs])
+        torch.cuda.synchronize()
+        print("ok", M, P, np.dtype(dt).name, kron.plan_describe(M, P, P, np.dtype(dt).name), float(Y.sum()))
+    ctx = kron.DistContext("virtual", GM=2, GK=2)
+    X = synth.matrix(4, 16 ** 3, 1, 0, "urand", np.float32)
+    blocks = [torch.from_numpy(np.ascontiguousarray(X[(r // 2) * 2:(r // 2) * 2 + 2, (r % 2) * 2048:(r % 2) * 2048 + 2048])).to(dev)
+              for r in range(4)]
+    Fs = [torch.from_numpy(f).to(dev) for f in synth.factors([16] * 3, [16] * 3, 1, "urand", np.float32)]
+    kron.matmul_dist(4, blocks, Fs, ctx)
+    torch.cuda.synchronize()
+    print("ok dist virtual 2x2")
+
+
+if __name__ == "__main__":
+    main()
