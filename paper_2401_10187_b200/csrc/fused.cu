@@ -859,22 +859,26 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
     unsigned char *buf = base + (size_t)st * a.stage_bytes;
 
     // ---------------- GEMM1: Z = X . F1 per chunk (warp-local, in place)
+    // swizzle bookkeeping: a row of P*ES bytes spans NL 128-byte lines; within a line the 128B TMA
+    // swizzle is an XOR of the in-line offset, so each access is one LOP3 on a per-row line base.
+    constexpr int NL = P * ES >= 128 ? P * ES / 128 : 1;
     for (int cg = warp; cg * CPG < nchunks; cg += NW) {
       const uint32_t gg = (uint32_t)(cg * CPG + c1);
       const uint32_t cbase = gg * C * ES;
       const uint32_t gx = pipe_gx<8, 4>(gg);
-      T acc[RM][RN];
+      uint32_t lb[RM][NL];
 #pragma unroll
       for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
+        for (int l = 0; l < NL; ++l) lb[i][l] = swz128(cbase + (uint32_t)(sg + (P / RM) * i) * (P * ES) + l * 128);
+      T acc[RM][RN];
 #pragma unroll 2
       for (int p0 = 0; p0 < P; p0 += VA) {
         T xa[RM][VA];
 #pragma unroll
         for (int i = 0; i < RM; ++i) {
-          const int s = sg + (P / RM) * i;
-          const unsigned char *src = buf + swz128(cbase + (uint32_t)(s * P + p0) * ES);
+          const uint32_t x = (uint32_t)p0 * ES;
+          const unsigned char *src = buf + (((NL > 1 && (x >> 7)) ? lb[i][NL - 1] : lb[i][0]) ^ (x & 127u));
           if constexpr (ES == 4) {
             const float4 v = *reinterpret_cast<const float4 *>(src);
             xa[i][0] = v.x; xa[i][1] = v.y; xa[i][2] = v.z; xa[i][3] = v.w;
@@ -897,19 +901,21 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
               f[j] = v.x; f[j + 1] = v.y;
             }
           }
+          const bool first = p0 == 0 && e == 0;
 #pragma unroll
           for (int i = 0; i < RM; ++i) {
             if constexpr (ES == 4) {
               const float2 xx = make_float2(xa[i][e], xa[i][e]);
 #pragma unroll
               for (int j = 0; j < RN; j += 2) {
-                const float2 r2 = __ffma2_rn(xx, make_float2(f[j], f[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+                const float2 ff = make_float2(f[j], f[j + 1]);
+                const float2 r2 = first ? __fmul2_rn(xx, ff) : __ffma2_rn(xx, ff, make_float2(acc[i][j], acc[i][j + 1]));
                 acc[i][j] = r2.x;
                 acc[i][j + 1] = r2.y;
               }
             } else {
 #pragma unroll
-              for (int j = 0; j < RN; ++j) acc[i][j] = fma(xa[i][e], f[j], acc[i][j]);
+              for (int j = 0; j < RN; ++j) acc[i][j] = first ? xa[i][e] * f[j] : fma(xa[i][e], f[j], acc[i][j]);
             }
           }
         }
@@ -917,10 +923,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
       __syncwarp();
 #pragma unroll
       for (int i = 0; i < RM; ++i) {
-        const int s = sg + (P / RM) * i;
 #pragma unroll
         for (int j = 0; j < RN; j += VA) {
-          unsigned char *dst = buf + (swz128(cbase + (uint32_t)(s * P + q1g * RN + j) * ES) ^ gx);
+          const uint32_t x = (uint32_t)(q1g * RN + j) * ES;
+          unsigned char *dst = buf + ((((NL > 1 && (x >> 7)) ? lb[i][NL - 1] : lb[i][0]) ^ (x & 127u)) ^ gx);
           if constexpr (ES == 4)
             *reinterpret_cast<float4 *>(dst) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
           else
@@ -937,14 +943,11 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
       const int oct = u2 / (U2_Q1 * U2_Q2), rest = u2 - oct * (U2_Q1 * U2_Q2);
       const int q1b = rest % U2_Q1, q2b = rest / U2_Q1;
       const uint32_t gg = (uint32_t)(oct * 8 + gl);
-      const uint32_t cbase = gg * C * ES;
       const uint32_t gx = pipe_gx<8, 4>(gg);
       const int q2base = (q2b * 4 + q2s) * RM, q1base = q1b * RN;
+      // Z row s, columns q1base..q1base+RN: a 32/64-byte aligned block inside one 128-byte line
+      const uint32_t zb0 = gg * C * ES + (uint32_t)q1base * ES;
       T acc[RM][RN];
-#pragma unroll
-      for (int i = 0; i < RM; ++i)
-#pragma unroll
-        for (int j = 0; j < RN; ++j) acc[i][j] = T(0);
 #pragma unroll 4
       for (int s = 0; s < P; ++s) {
         T fv[RM], zv[RN];
@@ -959,9 +962,10 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
             fv[i] = v.x; fv[i + 1] = v.y;
           }
         }
+        const uint32_t zrow = swz128(zb0 + (uint32_t)s * (P * ES)) ^ gx;
 #pragma unroll
         for (int j = 0; j < RN; j += VA) {
-          const unsigned char *src = buf + (swz128(cbase + (uint32_t)(s * P + q1base + j) * ES) ^ gx);
+          const unsigned char *src = buf + (zrow ^ (uint32_t)(j * ES));
           if constexpr (ES == 4) {
             const float4 v = *reinterpret_cast<const float4 *>(src);
             zv[j] = v.x; zv[j + 1] = v.y; zv[j + 2] = v.z; zv[j + 3] = v.w;
@@ -976,24 +980,27 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
             const float2 ff = make_float2(fv[i], fv[i]);
 #pragma unroll
             for (int j = 0; j < RN; j += 2) {
-              const float2 r2 = __ffma2_rn(ff, make_float2(zv[j], zv[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+              const float2 zz = make_float2(zv[j], zv[j + 1]);
+              const float2 r2 = s == 0 ? __fmul2_rn(ff, zz) : __ffma2_rn(ff, zz, make_float2(acc[i][j], acc[i][j + 1]));
               acc[i][j] = r2.x;
               acc[i][j + 1] = r2.y;
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < RN; ++j) acc[i][j] = fma(fv[i], zv[j], acc[i][j]);
+            for (int j = 0; j < RN; ++j) acc[i][j] = s == 0 ? fv[i] * zv[j] : fma(fv[i], zv[j], acc[i][j]);
           }
         }
       }
       // direct-index store: u = q2*P + q1 -> Y[row][u*(W/C) + cb*R + g]
       const int64_t gcol = (int64_t)cb * a.R + gg;
       if (gcol < a.WC && rb < a.M) {
-        T *yrow = Y + (int64_t)rb * a.Wout + gcol;
+        T *yb = Y + (int64_t)rb * a.Wout + gcol + (int64_t)(q2base * P + q1base) * a.WC;
 #pragma unroll
-        for (int i = 0; i < RM; ++i)
+        for (int i = 0; i < RM; ++i) {
+          T *yi = yb + (int64_t)(i * P) * a.WC;
 #pragma unroll
-          for (int j = 0; j < RN; ++j) yrow[(int64_t)((q2base + i) * P + q1base + j) * a.WC] = acc[i][j];
+          for (int j = 0; j < RN; ++j) yi[(int64_t)j * a.WC] = acc[i][j];
+        }
       }
     }
     __syncthreads();  // the stage is fully consumed
@@ -1032,7 +1039,7 @@ Kernel4Fn instance_kernel4(int i) {
   switch (i) {
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
-    case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 2>;
+    case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
     case 28: return kron_fused_gemm2_kernel<double, 32, 4, 8, 8, 1>;
   }
   return nullptr;
