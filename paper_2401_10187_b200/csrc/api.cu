@@ -2,6 +2,7 @@
 // fusion groups), the plan cache, workspace handling and dispatch.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -58,7 +59,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     // two-factor chunk GEMMs: exactly two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
   }
-  if (inst.warp == 2) {
+  if (inst.warp == 2 || inst.warp == 4) {
     if (k > 3) return false;                                   // one warp group per factor
     if (R % inst.rsw || (k >= 2 && C < (int64_t)inst.rsw * p)) return false;  // 16-byte chunk/slice vectors
     if (tileM * R / inst.rsw * (C / p) > 4 * inst.NT) return false;        // <= 4 last-step slots per thread
@@ -67,6 +68,10 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   int stages, nout = 0;
   if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
+  } else if (inst.warp == 4) {
+    if (tileM != 1) return false;
+    nout = 2;
+    stages = 4;  // two co-resident CTAs (one per pass) per SM
   } else if (inst.warp == 2) {
     nout = 2;
     stages = (int)((200 * 1024 - 2 * stage) / stage);  // deep ring: one CTA per SM
@@ -143,9 +148,11 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
     ++ip;
     if (pp.kind == KIND_FUSED) {
       if (!tmap_available()) return KRON_ERR_CUDA;
-      const void *grp[kMaxFused];
-      for (int i = 0; i < pp.nf; ++i) grp[i] = F[pp.first - 1 - i];
-      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, stream);
+      const void *grp[2 * kMaxFused];
+      const int nfac = pp.pair ? 2 * pp.nf : pp.nf;
+      for (int i = 0; i < nfac; ++i) grp[i] = F[pp.first - 1 - i];
+      void *aux = ws ? static_cast<char *>(ws) + (size_t)plan.nws * plan.ws_elems * es : nullptr;
+      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, aux, stream);
     } else if (pp.kind == KIND_GEMM) {
       err = launch_gemm(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
     } else {
@@ -158,7 +165,7 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
 }
 
 size_t ws_bytes_of(const Plan &plan) {
-  return (size_t)plan.nws * (size_t)plan.ws_elems * (size_t)es_of(plan.dtype);
+  return (size_t)plan.nws * (size_t)plan.ws_elems * (size_t)es_of(plan.dtype) + (size_t)plan.aux_bytes;
 }
 
 }  // namespace
@@ -277,6 +284,41 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     pp.kind = gemm_supported(dtype, Mp, W, p, q) ? KIND_GEMM : KIND_GENERIC;
     plan->passes.push_back(pp);
     f -= 1;
+  }
+
+  // L2-fused pairs (experimental): two consecutive factor-pipeline passes over the same width run as ONE cooperative
+  // launch; the first pass streams rows into a ring of NR rows that stays in L2 and the second pass
+  // consumes them a few rows behind, so the intermediate does not make an HBM round trip.
+  // Opt-in (KRON_PAIR=1): measured slower than two passes on config B in round 1 (each pass gets half an
+  // SM and the row hand-off polls), although the ring does keep ~60% of the intermediate out of HBM.
+  plan->aux_bytes = 0;
+  if (getenv("KRON_PAIR")) {
+    for (size_t i = 0; i + 1 < plan->passes.size(); ++i) {
+      const PassPlan &A = plan->passes[i], &B = plan->passes[i + 1];
+      if (A.kind != KIND_FUSED || B.kind != KIND_FUSED || fused_instance(A.variant).warp != 2 ||
+          fused_instance(B.variant).warp != 2 || A.nf != B.nf || A.P != B.P || A.W_in != B.W_in)
+        continue;
+      const int ip = fused_find(dtype, A.P, 4);
+      if (ip < 0) continue;
+      PassPlan pp;
+      if (!fused_geometry(fused_instance(ip), A.nf, A.W_in, Mp, &pp)) continue;
+      const int64_t es = es_of(dtype), row_bytes = A.W_in * es;
+      int64_t nr = (48ll << 20) / row_bytes;
+      if (nr > 32) nr = 32;
+      if (nr > M) nr = M;
+      if (nr < 4 || M < 2 * nr) continue;
+      pp.variant = ip;
+      pp.pair = 1;
+      pp.ring_rows = (int)nr;
+      pp.first = A.first;
+      pp.nf = A.nf;
+      pp.W_in = A.W_in;
+      pp.W_out = B.W_out;
+      plan->passes[i] = pp;
+      plan->passes.erase(plan->passes.begin() + i + 1);
+      plan->aux_bytes = nr * row_bytes + 2 * M * (int64_t)sizeof(int);
+      break;  // one ring per plan
+    }
   }
 
   // buffers (Alg 1, 318): the last pass writes Y, X is never written; interior
@@ -399,7 +441,7 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
   *npasses = (int32_t)plan.passes.size();
   for (int i = 0; i < (int)plan.passes.size() && i < cap; ++i) {
     if (first) first[i] = plan.passes[i].first;
-    if (nfactors) nfactors[i] = plan.passes[i].nf;
+    if (nfactors) nfactors[i] = plan.passes[i].pair ? 2 * plan.passes[i].nf : plan.passes[i].nf;
     if (kind) kind[i] = plan.passes[i].kind;
   }
   return KRON_OK;

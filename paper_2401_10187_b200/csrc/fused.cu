@@ -42,6 +42,13 @@ struct FusedArgs {
   int nslices;    // tileM * Sl
   int C;          // chunk = P^nf
   int nout;       // output buffers (warp-chain kernel): 2 = double-buffered TMA-store source
+  // L2-fused pair mode (factor-pipeline kernel): CTAs with odd blockIdx run the second pass of the
+  // pair, consuming rows of the first pass's output from a ring of NR rows that stays in L2
+  int pair;
+  const void *F2[kMaxFused];  // second-pass factors
+  int *produced;              // [M] tiles of row r written to the ring by the first pass
+  int *consumed;              // [M] tiles of row r loaded from the ring by the second pass
+  int NR;                     // ring rows
   void *Y;        // output matrix (kernels that store from registers)
   int64_t WC;     // W / C  (output column stride of a composite column u)
   int64_t Wout;   // output row width
@@ -569,12 +576,30 @@ struct VecIO<double, 2> {
 template <typename T, int P, int NWG, int VS, int G>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
-                                           int wg, int lane, int tid);
+                                           int wg, int lane, int tid, int role, int cta, int ncta);
+
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// spin (with back-off) until *p >= target
+__device__ __forceinline__ void wait_counter(const int *p, int target) {
+  if (ld_acquire(p) >= target) return;
+  unsigned ns = 64;
+  while (ld_acquire(p) < target) {
+    __nanosleep(ns);
+    if (ns < 1024) ns <<= 1;
+  }
+}
 
 template <typename T, int P, int NWG, int VS>
-__global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
+__global__ void __launch_bounds__(32 * (1 + NWG * 3), NWG == 2 ? 2 : 1)
     kron_fused_pipe_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                           const FusedArgs a) {
+                           const FusedArgs a, const __grid_constant__ CUtensorMap tm_in2,
+                           const __grid_constant__ CUtensorMap tm_out2) {
   constexpr int ES = sizeof(T);               // VS: consecutive slices (middle) / chunks (last) per thread
   constexpr int LINE = 128 / ES;
   constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
@@ -592,6 +617,11 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int nf = a.nf;
 
+  const int role = a.pair ? (int)(blockIdx.x & 1u) : 0;
+  const int cta = a.pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncta = a.pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const CUtensorMap *tin = role ? &tm_in2 : &tm_in;
+  const CUtensorMap *tout = role ? &tm_out2 : &tm_out;
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -599,8 +629,8 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
       for (int g = 0; g < MAXNF - 1; ++g) mbar_init(&done[g * a.stages + s], NWG * 32);
     }
     fence_mbar_init();
-    prefetch_tmap(&tm_in);
-    prefetch_tmap(&tm_out);
+    prefetch_tmap(tin);
+    prefetch_tmap(tout);
   }
   __syncthreads();
 
@@ -609,15 +639,24 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t tile = blockIdx.x, it = 0; tile < a.ntiles; tile += gridDim.x, ++it) {
+      for (int64_t tile = cta, it = 0; tile < a.ntiles; tile += ncta, ++it) {
         if (it >= a.stages) mbar_wait(&empty[st], ph ^ 1u);
         const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+        int lrow = rb * a.tileM;
+        if (a.pair) {
+          if (role == 0) {
+            if (rb >= a.NR) wait_counter(&a.consumed[rb - a.NR], a.tiles_k);  // ring slot is free
+          } else {
+            wait_counter(&a.produced[rb], a.tiles_k);  // the whole row of the first pass is in the ring
+            fence_proxy_async_global();
+            lrow = rb % a.NR;
+          }
+        }
         unsigned char *dst = base + (size_t)st * a.stage_bytes;
         mbar_arrive_expect_tx(&full[st], a.tile_bytes);
         const int line0 = cb * (a.tileK / LINE);
         for (int b = 0; b < a.nbox; ++b)
-          tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines,
-                      rb * a.tileM);
+          tma_load_3d(dst + (size_t)b * a.box_lines * 128, tin, &full[st], 0, line0 + b * a.box_lines, lrow);
         if (++st == a.stages) {
           st = 0;
           ph ^= 1u;
@@ -630,15 +669,15 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
   if (g >= nf) return;
   // one code path per group index so that the factor pointer (kernel parameter) and hence every
   // factor value is provably warp-uniform: the compiler keeps F in uniform registers
-  if (g == 0) pipe_group<T, P, NWG, VS, 0>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
-  else if (g == 1) pipe_group<T, P, NWG, VS, 1>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
-  else pipe_group<T, P, NWG, VS, 2>(a, &tm_out, base, obase, full, empty, done, wg, lane, tid);
+  if (g == 0) pipe_group<T, P, NWG, VS, 0>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  else if (g == 1) pipe_group<T, P, NWG, VS, 1>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  else pipe_group<T, P, NWG, VS, 2>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
 }
 
 template <typename T, int P, int NWG, int VS, int G>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
-                                           int wg, int lane, int tid) {
+                                           int wg, int lane, int tid, int role, int cta, int ncta) {
   constexpr int ES = sizeof(T);
   constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
   constexpr int EPV = 16 / ES > P ? P : 16 / ES;
@@ -646,7 +685,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   const int g = G, nf = a.nf;
   // this group's factor F_{first-g} lives in (uniform) registers for the whole kernel
   RegFactor<T, P> Fr;
-  Fr.load(reinterpret_cast<const T *>(a.F[G]));
+  Fr.load(reinterpret_cast<const T *>(role ? a.F2[G] : a.F[G]));
   const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
   const uint32_t tile_elems = (uint32_t)a.tileM * (uint32_t)a.tileK;
   const bool gx_on = C * ES >= 128;  // the granule XOR must be constant over each 128-byte line
@@ -659,8 +698,13 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
     const uint32_t nreg = tile_elems / GE;
     int st = 0;
     uint32_t ph = 0;
-    for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x) {
+    for (int64_t tile = cta; tile < a.ntiles; tile += ncta) {
       mbar_wait(g == 0 ? &full[st] : &done[(g - 1) * a.stages + st], ph);
+      if (a.pair && role == 1 && g == 0 && wg == 0 && lane == 0) {
+        // the tile has left the ring (TMA bytes landed): count it for the first pass's back-pressure
+        __threadfence();
+        atomicAdd(&a.consumed[tile / a.tiles_k], 1);
+      }
       unsigned char *buf = base + (size_t)st * a.stage_bytes;
 #pragma unroll 1
       for (uint32_t grp = (uint32_t)wg; grp < nreg; grp += NWG) {
@@ -729,7 +773,9 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   }
   int st = 0;
   uint32_t ph = 0;
-  for (int64_t tile = blockIdx.x, it = 0; tile < a.ntiles; tile += gridDim.x, ++it) {
+  const bool signal = a.pair && role == 0;  // first pass of a pair: publish finished ring rows
+  int64_t prev_row = -1;
+  for (int64_t tile = cta, it = 0; tile < a.ntiles; tile += ncta, ++it) {
     mbar_wait(nf == 1 ? &full[st] : &done[(nf - 2) * a.stages + st], ph);
     named_bar_sync(1, LT);  // the store that last read this output buffer has finished reading it
     const unsigned char *buf = base + (size_t)st * a.stage_bytes;
@@ -774,16 +820,33 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
     if (lt == 0) {
       mbar_arrive(&empty[st]);  // every group is done with this stage
       const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
-      tma_store_4d(tm_out, obuf, cb * a.R, 0, 0, rb * a.tileM);
+      tma_store_4d(tm_out, obuf, cb * a.R, 0, 0, signal ? rb % a.NR : rb * a.tileM);
       bulk_commit();
-      bulk_wait_read<1>();
+      if (signal) {
+        bulk_wait<1>();  // the previous tile's store has completed: publish its row
+        if (prev_row >= 0) {
+          fence_proxy_async_global();
+          __threadfence();
+          atomicAdd(&a.produced[prev_row], 1);
+        }
+        prev_row = rb;
+      } else {
+        bulk_wait_read<1>();
+      }
     }
     if (++st == a.stages) {
       st = 0;
       ph ^= 1u;
     }
   }
-  if (lt == 0) bulk_wait<0>();
+  if (lt == 0) {
+    bulk_wait<0>();
+    if (signal && prev_row >= 0) {
+      fence_proxy_async_global();
+      __threadfence();
+      atomicAdd(&a.produced[prev_row], 1);
+    }
+  }
 }
 
 // ------------------------------------------------------------------ two-factor GEMM chunks (v4)
@@ -1029,10 +1092,13 @@ const FusedInstance kInstances[] = {
     // v4: two-factor chunk GEMMs (tile = 256 * RS * P elements = 8192)
     {KRON_F32, 16, 256, 2, 3, 0}, {KRON_F32, 32, 256, 1, 3, 0},
     {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
+    // L2-fused pair of factor pipelines (two passes in one cooperative launch): id 29
+    {KRON_F32, 8, 64, 8, 4, 2},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs);
+using KernelPFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs, const CUtensorMap, const CUtensorMap);
 using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
@@ -1045,13 +1111,20 @@ Kernel4Fn instance_kernel4(int i) {
   return nullptr;
 }
 
-KernelFn instance_kernel(int i) {
+KernelPFn instance_pipe(int i) {
   switch (i) {
     case 0: return kron_fused_pipe_kernel<float, 2, 4, 4>;
     case 1: return kron_fused_pipe_kernel<float, 4, 4, 4>;
     case 2: return kron_fused_pipe_kernel<float, 8, 4, 2>;
     case 3: return kron_fused_pipe_kernel<double, 2, 4, 2>;
     case 4: return kron_fused_pipe_kernel<double, 4, 4, 2>;
+    case 29: return kron_fused_pipe_kernel<float, 8, 2, 2>;
+  }
+  return nullptr;
+}
+
+KernelFn instance_kernel(int i) {
+  switch (i) {
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
     case 7: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
@@ -1118,7 +1191,7 @@ int fused_find(int dtype, int P, int warp) {
 }
 
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *stream) {
+                 void *aux, void *stream) {
   const FusedInstance &inst = kInstances[pp.variant];
   const int es = dtype == KRON_F32 ? 4 : 8;
   const int line = 128 / es;
@@ -1158,6 +1231,26 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     if (!encode_tmap(&tout, dtype, 4, out, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
   }
 
+  CUtensorMap tin2 = tin, tout2 = tout;
+  if (inst.warp == 4) {
+    // L2-fused pair: pass 1 writes a ring of NR rows (aux), pass 2 reads it; per-row counters follow
+    a.pair = 1;
+    a.NR = pp.ring_rows;
+    for (int i = 0; i < pp.nf; ++i) a.F2[i] = Fgroup[pp.nf + i];
+    a.produced = reinterpret_cast<int *>(static_cast<char *>(aux) + (size_t)pp.ring_rows * W * es);
+    a.consumed = a.produced + M;
+    const int64_t qlo = pp.Qc > 256 ? 256 : pp.Qc, qhi = pp.Qc / qlo;
+    uint64_t d1[4] = {(uint64_t)WC, (uint64_t)qlo, (uint64_t)qhi, (uint64_t)pp.ring_rows};
+    uint64_t s1[3] = {(uint64_t)WC * es, (uint64_t)(WC * qlo * es), (uint64_t)W * es};
+    uint32_t b1[4] = {(uint32_t)pp.R, (uint32_t)qlo, (uint32_t)qhi, 1};
+    if (!encode_tmap(&tout, dtype, 4, aux, d1, s1, b1, false)) return (int)cudaErrorInvalidValue;
+    uint64_t d2[3] = {(uint64_t)line, (uint64_t)(W / line), (uint64_t)pp.ring_rows};
+    uint64_t s2[2] = {128, (uint64_t)W * es};
+    uint32_t b2[3] = {(uint32_t)line, (uint32_t)a.box_lines, 1};
+    if (!encode_tmap(&tin2, dtype, 3, aux, d2, s2, b2, true)) return (int)cudaErrorInvalidValue;
+    if (cudaMemsetAsync(a.produced, 0, 2 * (size_t)M * sizeof(int), (cudaStream_t)stream) != cudaSuccess)
+      return (int)cudaGetLastError();
+  }
   a.nout = pp.nout;
   a.Y = out;
   a.WC = WC;
@@ -1167,7 +1260,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   int threads = inst.NT;
   if (inst.warp == 3) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
-  } else if (inst.warp == 2) {
+  } else if (inst.warp == 2 || inst.warp == 4) {
     smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
     threads = 32 * (1 + 3 * (inst.NT / 32));  // producer warp + one warp group per factor (max 3)
   } else {
@@ -1189,6 +1282,40 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     if (grid > a.ntiles) grid = a.ntiles;
     k4<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, a);
     return (int)cudaGetLastError();
+  }
+  if (inst.warp == 2 || inst.warp == 4) {
+    KernelPFn kp = instance_pipe(pp.variant);
+    cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, threads, smem);
+    if (e != cudaSuccess) return (int)e;
+    if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (inst.warp == 2) {
+      int64_t grid = (int64_t)sms * per_sm;
+      if (grid > a.ntiles) grid = a.ntiles;
+      kp<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a, tin2, tout2);
+      return (int)cudaGetLastError();
+    }
+    // pair: both passes co-resident (cooperative launch), one CTA of each role per slot
+    int64_t half = (int64_t)sms * per_sm / 2;
+    if (half > a.ntiles) half = a.ntiles;
+    if (half < 1) return (int)cudaErrorInvalidConfiguration;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)(2 * half));
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = (cudaStream_t)stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kp, tin, tout, a, tin2, tout2);
+    return (int)e;
   }
   KernelFn k = instance_kernel(pp.variant);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -30,6 +30,8 @@ struct PassPlan {
   int variant = -1;  // fused: kernel instance id; gemm: instance id
   int stages = 2;
   int nout = 0;  // output staging buffers (warp-chain fused kernel)
+  int pair = 0;       // 1: L2-fused pair of passes (factors first .. first-2nf+1), one cooperative launch
+  int ring_rows = 0;  // pair: rows of the L2-resident ring between the two passes
   int src = BUF_X, dst = BUF_Y;
 };
 
@@ -41,6 +43,7 @@ struct Plan {
   std::vector<PassPlan> passes;
   int nws = 0;             // workspace buffers (0, 1 or 2)
   int64_t ws_elems = 0;    // elements per workspace buffer
+  int64_t aux_bytes = 0;   // extra workspace after the buffers (L2-fused pair: ring + row counters)
 };
 
 // Builds the plan (host only).  Returns KRON_OK or a validation error.
@@ -70,7 +73,7 @@ int fused_find(int dtype, int P, int warp);  // instance id or -1
 int launch_generic(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F,
                    void *stream);
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *stream);
+                 void *aux, void *stream);
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 

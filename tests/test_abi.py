@@ -103,6 +103,19 @@ def test_workspace_sizes(kron):
     assert ws >= 10 * 64 * 8
 
 
+def test_l2_pair_plan_opt_in():
+    # the experimental L2-fused pair (KRON_PAIR=1) plans one launch for both groups of config B with a
+    # 32-row ring; checked in a fresh process because plans are cached per process
+    import subprocess
+    import sys
+    code = ("from paper_2401_10187_b200 import kron; "
+            "print(kron.plan_describe(1024,[8]*6,[8]*6,'float32'), kron.workspace_size(1024,[8]*6,[8]*6,'float32'), "
+            "kron.plan_cost(1024,[8]*6,[8]*6,'float32')[0])")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
+                         env={**os.environ, "KRON_PAIR": "1"}).stdout.strip()
+    assert out == f"[(6, 6, 'fused')] {32 * 8 ** 6 * 4 + 2 * 1024 * 4} {float(2 * 4 * 1024 * 8 ** 6 + 6 * 4 * 64)}"
+
+
 def test_grid_rule_matches_oracle(kron):
     for G in [1, 2, 4, 8, 16, 32, 64]:
         assert kron.grid_rule(G) == oracle.grid(G)
