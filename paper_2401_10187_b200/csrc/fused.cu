@@ -573,7 +573,7 @@ struct VecIO<double, 2> {
   }
 };
 
-template <typename T, int P, int NWG, int VS, int G>
+template <typename T, int P, int NWG, int VS, int G, bool PAIR>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
                                            int wg, int lane, int tid, int role, int cta, int ncta);
@@ -595,8 +595,8 @@ __device__ __forceinline__ void wait_counter(const int *p, int target) {
   }
 }
 
-template <typename T, int P, int NWG, int VS>
-__global__ void __launch_bounds__(32 * (1 + NWG * 3), NWG == 2 ? 2 : 1)
+template <typename T, int P, int NWG, int VS, bool PAIR>
+__global__ void __launch_bounds__(32 * (1 + NWG * 3), PAIR ? 2 : 1)
     kron_fused_pipe_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
                            const FusedArgs a, const __grid_constant__ CUtensorMap tm_in2,
                            const __grid_constant__ CUtensorMap tm_out2) {
@@ -617,11 +617,11 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), NWG == 2 ? 2 : 1)
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int nf = a.nf;
 
-  const int role = a.pair ? (int)(blockIdx.x & 1u) : 0;
-  const int cta = a.pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int ncta = a.pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const CUtensorMap *tin = role ? &tm_in2 : &tm_in;
-  const CUtensorMap *tout = role ? &tm_out2 : &tm_out;
+  const int role = PAIR ? (int)(blockIdx.x & 1u) : 0;
+  const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const CUtensorMap *tin = (PAIR && role) ? &tm_in2 : &tm_in;
+  const CUtensorMap *tout = (PAIR && role) ? &tm_out2 : &tm_out;
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), NWG == 2 ? 2 : 1)
         if (it >= a.stages) mbar_wait(&empty[st], ph ^ 1u);
         const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
         int lrow = rb * a.tileM;
-        if (a.pair) {
+        if constexpr (PAIR) {
           if (role == 0) {
             if (rb >= a.NR) wait_counter(&a.consumed[rb - a.NR], a.tiles_k);  // ring slot is free
           } else {
@@ -669,12 +669,12 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), NWG == 2 ? 2 : 1)
   if (g >= nf) return;
   // one code path per group index so that the factor pointer (kernel parameter) and hence every
   // factor value is provably warp-uniform: the compiler keeps F in uniform registers
-  if (g == 0) pipe_group<T, P, NWG, VS, 0>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
-  else if (g == 1) pipe_group<T, P, NWG, VS, 1>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
-  else pipe_group<T, P, NWG, VS, 2>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  if (g == 0) pipe_group<T, P, NWG, VS, 0, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  else if (g == 1) pipe_group<T, P, NWG, VS, 1, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  else pipe_group<T, P, NWG, VS, 2, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
 }
 
-template <typename T, int P, int NWG, int VS, int G>
+template <typename T, int P, int NWG, int VS, int G, bool PAIR>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
                                            int wg, int lane, int tid, int role, int cta, int ncta) {
@@ -685,7 +685,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   const int g = G, nf = a.nf;
   // this group's factor F_{first-g} lives in (uniform) registers for the whole kernel
   RegFactor<T, P> Fr;
-  Fr.load(reinterpret_cast<const T *>(role ? a.F2[G] : a.F[G]));
+  Fr.load(reinterpret_cast<const T *>((PAIR && role) ? a.F2[G] : a.F[G]));
   const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
   const uint32_t tile_elems = (uint32_t)a.tileM * (uint32_t)a.tileK;
   const bool gx_on = C * ES >= 128;  // the granule XOR must be constant over each 128-byte line
@@ -700,7 +700,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
     uint32_t ph = 0;
     for (int64_t tile = cta; tile < a.ntiles; tile += ncta) {
       mbar_wait(g == 0 ? &full[st] : &done[(g - 1) * a.stages + st], ph);
-      if (a.pair && role == 1 && g == 0 && wg == 0 && lane == 0) {
+      if (PAIR && role == 1 && g == 0 && wg == 0 && lane == 0) {
         // the tile has left the ring (TMA bytes landed): count it for the first pass's back-pressure
         __threadfence();
         atomicAdd(&a.consumed[tile / a.tiles_k], 1);
@@ -773,7 +773,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   }
   int st = 0;
   uint32_t ph = 0;
-  const bool signal = a.pair && role == 0;  // first pass of a pair: publish finished ring rows
+  const bool signal = PAIR && role == 0;  // first pass of a pair: publish finished ring rows
   int64_t prev_row = -1;
   for (int64_t tile = cta, it = 0; tile < a.ntiles; tile += ncta, ++it) {
     mbar_wait(nf == 1 ? &full[st] : &done[(nf - 2) * a.stages + st], ph);
@@ -1113,12 +1113,12 @@ Kernel4Fn instance_kernel4(int i) {
 
 KernelPFn instance_pipe(int i) {
   switch (i) {
-    case 0: return kron_fused_pipe_kernel<float, 2, 4, 4>;
-    case 1: return kron_fused_pipe_kernel<float, 4, 4, 4>;
-    case 2: return kron_fused_pipe_kernel<float, 8, 4, 2>;
-    case 3: return kron_fused_pipe_kernel<double, 2, 4, 2>;
-    case 4: return kron_fused_pipe_kernel<double, 4, 4, 2>;
-    case 29: return kron_fused_pipe_kernel<float, 8, 2, 2>;
+    case 0: return kron_fused_pipe_kernel<float, 2, 4, 4, false>;
+    case 1: return kron_fused_pipe_kernel<float, 4, 4, 4, false>;
+    case 2: return kron_fused_pipe_kernel<float, 8, 4, 2, false>;
+    case 3: return kron_fused_pipe_kernel<double, 2, 4, 2, false>;
+    case 4: return kron_fused_pipe_kernel<double, 4, 4, 2, false>;
+    case 29: return kron_fused_pipe_kernel<float, 8, 2, 2, true>;
   }
   return nullptr;
 }
