@@ -208,6 +208,69 @@ def run_reference(args, cfg_name):
     return 0
 
 
+# Paper workload sweeps (shapes only, synthetic data): Table 3 (M = 16, largest P^N, float and double,
+# P:997-1013) and Table 4 (28 real-world sizes).  "a^n x b^n" = n factors of a x b.
+TABLE3 = [(16, [8] * 8, [8] * 8), (16, [16] * 6, [16] * 6), (16, [32] * 5, [32] * 5), (16, [64] * 4, [64] * 4)]
+TABLE4 = [
+    (20, [2] * 7, [2] * 7), (20, [2] * 9, [2] * 9), (50, [2] * 9, [2] * 9), (20, [2] * 10, [2] * 10),
+    (1, [2] * 11, [2] * 11),
+    (10, [52, 65], [50, 20]), (50, [32, 64], [8, 128]), (10, [52, 50], [65, 20]),
+    (4, [2] * 9, [2] * 9), (8, [2] * 9, [2] * 9), (16, [2] * 9, [2] * 9), (20, [2] * 9, [2] * 9),
+    (4, [8] * 3, [8] * 3), (8, [8] * 3, [8] * 3), (16, [8] * 3, [8] * 3), (20, [8] * 3, [8] * 3),
+    (1024, [3] * 7, [3] * 7), (1024, [4] * 7, [4] * 7), (1024, [6] * 7, [6] * 7),
+    (1, [5] * 3 + [2], [5] * 3 + [2]), (1, [5] * 2 + [2, 25], [5] * 2 + [2, 25]),
+    (1526, [4] * 6, [4] * 6), (156, [8] * 3, [8] * 3), (2967, [4] * 7, [4] * 7),
+    (16, [8] * 8, [8] * 8), (16, [16] * 6, [16] * 6), (16, [32] * 6, [32] * 6), (16, [64] * 3, [64] * 3),
+]
+
+
+def run_sweep(args):
+    """One JSON line per shape: device-resident GFLOP/s of kron_matmul_ws (CUDA events, mean of steps)."""
+    import torch
+    import synth
+    from paper_2401_10187_b200 import kron
+    dev = torch.device("cuda", 0)
+    shapes = TABLE3 if args.sweep == "table3" else TABLE4
+    dts = ["float32", "float64"] if args.sweep == "table3" else ["float32"]
+    free = torch.cuda.mem_get_info()[0]
+    for idx, (M, P, Q) in enumerate(shapes):
+        for dtn in dts:
+            tdt = getattr(torch, dtn)
+            es = 4 if dtn == "float32" else 8
+            K, L = int(np.prod(P)), int(np.prod(Q))
+            wsz = kron.workspace_size(M, P, Q, tdt)
+            need = M * (K + L) * es + wsz
+            line = {"sweep": args.sweep, "id": idx + 1, "M": M, "P": P, "Q": Q, "dtype": dtn,
+                    "plan": [list(p) for p in kron.plan_describe(M, P, Q, tdt)]}
+            if need > 0.9 * free:
+                line["skipped"] = f"needs {need / 2**30:.1f} GiB"
+                print(json.dumps(line), flush=True)
+                continue
+            X = torch.empty((M, K), dtype=tdt, device=dev)
+            synth.fill_device(X.data_ptr(), M, K, synth.SEED_BASE + 50 + idx, 0, "urand", np.dtype(dtn))
+            Fs = [torch.from_numpy(f).to(dev) for f in synth.factors(P, Q, synth.SEED_BASE + 50 + idx, "urand",
+                                                                       np.dtype(dtn))]
+            Y = torch.empty((M, L), dtype=tdt, device=dev)
+            work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
+            for _ in range(args.warmup):
+                kron.matmul_ws(X, Fs, Y, work)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(args.steps):
+                kron.matmul_ws(X, Fs, Y, work)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            fl = flops_of(M, P, Q)
+            b_alg, _ = kron.plan_cost(M, P, Q, tdt)
+            line.update({"ms": round(ms, 5), "gflops": round(fl / ms / 1e6, 2), "hbm_gbs": round(b_alg / ms / 1e6, 1)})
+            print(json.dumps(line), flush=True)
+            del X, Y, work, Fs
+            torch.cuda.empty_cache()
+    return 0
+
+
 def run_dist(args, ws, rank, local, dev, barrier):
     """Strong scaling of one configuration over a {GM,GK} grid with kron_matmul_dist (NCCL)."""
     import torch
@@ -295,12 +358,16 @@ def main():
                     help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
                          "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
     ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
+    ap.add_argument("--sweep", default=None, choices=["table3", "table4"],
+                    help="paper shape sweeps (one JSON line per shape) instead of the headline bench")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
 
     if args.impl == "reference":
         return run_reference(args, args.config)
+    if args.sweep:
+        return run_sweep(args)
 
     import torch
     import synth

@@ -53,6 +53,10 @@ typedef enum {
 /* Human-readable name of a status code (static storage; never NULL). */
 const char *kron_status_string(kron_status_t s);
 
+/* Detail of the most recent KRON_ERR_CUDA / KRON_ERR_NCCL returned on the calling thread (the CUDA or
+ * NCCL error name and the failing step), or "" if none.  Thread-local static storage.            */
+const char *kron_last_error_detail(void);
+
 /* ---------------------------------------------------------------------------------------------
  * Single GPU — Algorithm 1 + fusion.
  *

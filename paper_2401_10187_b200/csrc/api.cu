@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -134,6 +135,13 @@ kron_status_t cached_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, 
   return KRON_OK;
 }
 
+thread_local char g_err_detail[256] = "";
+
+kron_status_t cuda_fail(int err, const char *what) {
+  snprintf(g_err_detail, sizeof(g_err_detail), "%s: %s", what, cudaGetErrorName((cudaError_t)err));
+  return KRON_ERR_CUDA;
+}
+
 kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
                        void *const *events = nullptr) {
   const size_t es = es_of(plan.dtype);
@@ -158,7 +166,9 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
     } else {
       err = launch_generic(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
     }
-    if (err != 0) return KRON_ERR_CUDA;
+    if (err != 0)
+      return cuda_fail(err, pp.kind == KIND_FUSED ? "fused pass launch"
+                            : pp.kind == KIND_GEMM ? "gemm pass launch" : "generic pass launch");
   }
   if (events && cudaEventRecord((cudaEvent_t)events[ip], (cudaStream_t)stream) != cudaSuccess) return KRON_ERR_CUDA;
   return KRON_OK;
@@ -346,6 +356,8 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
 using namespace kron;
 
 extern "C" {
+
+const char *kron_last_error_detail(void) { return g_err_detail; }
 
 const char *kron_status_string(kron_status_t s) {
   switch (s) {

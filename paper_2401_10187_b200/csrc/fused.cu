@@ -24,7 +24,9 @@
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <type_traits>
 
 #include "kron_internal.h"
@@ -1182,6 +1184,34 @@ bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const u
   return r == CUDA_SUCCESS;
 }
 
+
+// Host-side launch bookkeeping is cached per (kernel, block, smem): cudaFuncSetAttribute and the
+// occupancy query cost microseconds, which dominate small problems (Table 4 sizes).
+int kernel_slots(const void *fn, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<const void *, int, size_t, int>, int> cache;
+  static std::map<std::pair<const void *, int>, size_t> attr;  // dynamic-smem limit set per (kernel, device)
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(fn, threads, smem, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  // the attribute only ever grows, so launches with any smaller smem stay valid
+  size_t &cur = attr[std::make_pair(fn, dev)];
+  if (smem > cur) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
+    cur = smem;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return -1;
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int slots = per_sm * sms;
+  cache[key] = slots;
+  return slots;
+}
+
 int fused_instance_count() { return kNumInstances; }
 const FusedInstance &fused_instance(int i) { return kInstances[i]; }
 int fused_find(int dtype, int P, int warp) {
@@ -1269,39 +1299,25 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   }
   if (inst.warp == 3) {
     Kernel4Fn k4 = instance_kernel4(pp.variant);
-    cudaError_t e = cudaFuncSetAttribute(k4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k4, threads, smem);
-    if (e != cudaSuccess) return (int)e;
-    if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int64_t grid = (int64_t)sms * per_sm;
+    const int slots = kernel_slots((const void *)k4, threads, smem);
+    if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+    int64_t grid = slots;
     if (grid > a.ntiles) grid = a.ntiles;
     k4<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, a);
     return (int)cudaGetLastError();
   }
   if (inst.warp == 2 || inst.warp == 4) {
     KernelPFn kp = instance_pipe(pp.variant);
-    cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
-    int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kp, threads, smem);
-    if (e != cudaSuccess) return (int)e;
-    if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int slots = kernel_slots((const void *)kp, threads, smem);
+    if (slots < 1) return (int)cudaErrorInvalidConfiguration;
     if (inst.warp == 2) {
-      int64_t grid = (int64_t)sms * per_sm;
+      int64_t grid = slots;
       if (grid > a.ntiles) grid = a.ntiles;
       kp<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a, tin2, tout2);
       return (int)cudaGetLastError();
     }
     // pair: both passes co-resident (cooperative launch), one CTA of each role per slot
-    int64_t half = (int64_t)sms * per_sm / 2;
+    int64_t half = slots / 2;
     if (half > a.ntiles) half = a.ntiles;
     if (half < 1) return (int)cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg{};
@@ -1314,20 +1330,12 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     attr[0].val.cooperative = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, kp, tin, tout, a, tin2, tout2);
-    return (int)e;
+    return (int)cudaLaunchKernelEx(&cfg, kp, tin, tout, a, tin2, tout2);
   }
   KernelFn k = instance_kernel(pp.variant);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem);
-  if (e != cudaSuccess) return (int)e;
-  if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = (int64_t)sms * per_sm;
+  const int slots = kernel_slots((const void *)k, threads, smem);
+  if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+  int64_t grid = slots;
   if (grid > a.ntiles) grid = a.ntiles;
   k<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a);
   return (int)cudaGetLastError();

@@ -379,12 +379,9 @@ int launch_dmma(const PassPlan &pp, int64_t M, const void *in, void *out, const 
   }
   const size_t smem = 1024 + NS * ((size_t)BM * BK * 8 + (size_t)BK * BN * 8) + 16 * NS;
   auto k = kron_dmma_kernel<NWARP, NS>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = sms;
+  const int slots = kernel_slots((const void *)k, (NWARP + 1) * 32, smem);
+  if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+  int64_t grid = slots;
   if (grid > g.ntiles) grid = g.ntiles;
   k<<<(unsigned)grid, (NWARP + 1) * 32, smem, (cudaStream_t)stream>>>(ta, tb, (double *)out, g);
   return (int)cudaGetLastError();
@@ -433,16 +430,9 @@ int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *
   const size_t stage = (size_t)gs.BM * BK * es + (size_t)BK * gs.BN * es;
   const size_t smem = 1024 + gs.NS * stage + 8 * gs.NS;
   GemmFn k = gemm_kernel(gi);
-  cudaError_t e = cudaFuncSetAttribute((const void *)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return (int)e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void *)k, 256, smem);
-  if (e != cudaSuccess) return (int)e;
-  if (per_sm < 1) return (int)cudaErrorInvalidConfiguration;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int64_t grid = (int64_t)sms * per_sm;
+  const int slots = kernel_slots((const void *)k, 256, smem);
+  if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+  int64_t grid = slots;
   if (grid > g.ntiles) grid = g.ntiles;
   k<<<(unsigned)grid, 256, smem, (cudaStream_t)stream>>>(ta, tb, out, g);
   return (int)cudaGetLastError();

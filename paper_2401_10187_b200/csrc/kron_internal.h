@@ -77,6 +77,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 
+// resident CTA slots (SMs x CTAs per SM) for a kernel launch shape; sets the dynamic-smem attribute.
+// Cached per (kernel, block, smem, device).  fused.cu
+int kernel_slots(const void *fn, int threads, size_t smem);
+
 // tensor-map encoder (driver entry point fetched through the runtime); fused.cu
 bool tmap_available();
 bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims, const uint64_t *strides,

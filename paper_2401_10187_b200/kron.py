@@ -23,6 +23,8 @@ STATUS = {0: "KRON_OK", 1: "KRON_ERR_INVALID_ARG", 2: "KRON_ERR_SHAPE", 3: "KRON
 
 _lib.kron_status_string.restype = ctypes.c_char_p
 _lib.kron_status_string.argtypes = [ctypes.c_int]
+_lib.kron_last_error_detail.restype = ctypes.c_char_p
+_lib.kron_last_error_detail.argtypes = []
 _lib.kron_matmul.restype = ctypes.c_int
 _lib.kron_matmul.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
                              ctypes.c_int, ctypes.c_void_p]
@@ -54,7 +56,8 @@ KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm"}
 class KronError(RuntimeError):
     def __init__(self, code: int, what: str):
         self.code = code
-        super().__init__(f"{what}: {STATUS.get(code, code)}")
+        detail = _lib.kron_last_error_detail().decode() if code in (5, 6) else ""
+        super().__init__(f"{what}: {STATUS.get(code, code)}" + (f" ({detail})" if detail else ""))
 
 
 def _check(rc: int, what: str) -> None:
