@@ -56,7 +56,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   if (tileM > 1 && lines > 256) return false;
   if (C > 256 && (C % 256 || C / 256 > 256)) return false;
   if (inst.warp && ((int64_t)32 * inst.rsw * p) % C) return false;  // warp share = whole chunks
-  if (inst.warp == 3) {
+  if (inst.warp == 3 || inst.warp == 5) {
     // two-factor chunk GEMMs: exactly two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
   }
@@ -67,7 +67,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 3) {
+  if (inst.warp == 3 || inst.warp == 5) {
     stages = stage <= 32 * 1024 ? 3 : 2;
   } else if (inst.warp == 4) {
     if (tileM != 1) return false;
@@ -246,6 +246,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
   while (f >= 1) {
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
+    const int inst_d = (p == q && !getenv("KRON_NO_DMMA")) ? fused_find(dtype, p, 5) : -1;
     const int inst_g = (p == q) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q) ? fused_find(dtype, p, 1) : -1;
@@ -255,6 +256,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_d >= 0 && fused_geometry(fused_instance(inst_d), k, W, Mp, pp)) return inst_d;
         if (inst_g >= 0 && fused_geometry(fused_instance(inst_g), k, W, Mp, pp)) return inst_g;
         if (inst_p >= 0 && fused_geometry(fused_instance(inst_p), k, W, Mp, pp)) return inst_p;
         if (inst_w >= 0 && fused_geometry(fused_instance(inst_w), k, W, Mp, pp)) return inst_w;

@@ -1073,6 +1073,159 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
   }
 }
 
+// ------------------------------------------------------------------ fp64 two-factor chunks on DMMA (v5)
+//
+// The v4 sandwich OUT = F2^T . (X . F1) per 32 x 32 chunk, fp64, on the FP64 tensor cores (mma.sync
+// m16n8k4, SASS DMMA — tcgen05 has no f64 kind).  A warp owns a chunk: GEMM1 (64 DMMA) reads X rows
+// from the TMA tile and F1 from shared memory, writes Z in place; GEMM2 (64 DMMA) reads F2^T and Z and
+// writes OUT[q2][q1] in place.  All [32][32] fp64 matrices use 256-byte rows with the 128B swizzle on
+// each 128-byte line, which makes every fragment gather bank-conflict free.  A CTA-wide pass then
+// streams OUT chunk-fastest to Y[row][u*(W/C) + g0 + g]: 8 consecutive chunks = 64-byte runs.
+__device__ __forceinline__ uint32_t rowswz32(uint32_t r, uint32_t c) {  // [rows][32 doubles], byte offset
+  const uint32_t line = 2u * r + (c >> 4);
+  return line * 128u + (((c & 15u) << 3) ^ ((line & 7u) << 4));
+}
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                     const FusedArgs a) {
+  constexpr int P = 32, C = P * P, LINE = 16;
+  constexpr uint32_t CB = C * 8;  // chunk bytes
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char *F1s = base + (size_t)a.stages * a.stage_bytes;  // [p][q1]
+  unsigned char *F2Ts = F1s + CB;                                 // [q2][s] = F2[s][q2]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(F2Ts + CB);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+
+  {
+    const double *F1 = reinterpret_cast<const double *>(a.F[0]);
+    const double *F2 = reinterpret_cast<const double *>(a.F[1]);
+    for (int i = tid; i < C; i += NW * 32) {
+      const uint32_t r = (uint32_t)i / P, c = (uint32_t)i % P;
+      *reinterpret_cast<double *>(F1s + rowswz32(r, c)) = F1[i];   // F1[p = r][q1 = c]
+      *reinterpret_cast<double *>(F2Ts + rowswz32(c, r)) = F2[i];  // F2[s = r][q2 = c] -> F2T[c][r]
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  const int nchunks = a.R;  // tileM == 1
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * a.stage_bytes;
+    mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
+    const int line0 = cb * (a.tileK / LINE);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+  double *Y = reinterpret_cast<double *>(a.Y);
+
+  for (int it = 0;; ++it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) break;
+    const int st = it % a.stages;
+    mbar_wait(&bars[st], (uint32_t)((it / a.stages) & 1));
+    unsigned char *buf = base + (size_t)st * a.stage_bytes;
+
+    for (int g = warp; g < nchunks; g += NW) {
+      unsigned char *cb0 = buf + (uint32_t)g * CB;
+      const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
+      double acc[2][4][4];
+      // ---- GEMM1: Z[s][q1] = sum_p X[s][p] F1[p][q1]
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < P; k0 += 4) {
+        double a0[2], a1[2], b[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          a0[mt] = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq, k0 + tq));
+          a1[mt] = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq + 8, k0 + tq));
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(F1s + rowswz32(k0 + tq, nt * 8 + gq));
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[mt][nt], a0[mt], a1[mt], b[nt]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int v1 = 0; v1 < 2; ++v1)
+            *reinterpret_cast<double2 *>(cb0 + rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+                make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
+      __syncwarp();
+      // ---- GEMM2: OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < P; k0 += 4) {
+        double a0[2], a1[2], b[4];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt) {
+          a0[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq, k0 + tq));
+          a1[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq + 8, k0 + tq));
+        }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswz32(k0 + tq, nt * 8 + gq));
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[mt][nt], a0[mt], a1[mt], b[nt]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int v1 = 0; v1 < 2; ++v1)
+            *reinterpret_cast<double2 *>(cb0 + (rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
+                make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
+      __syncwarp();
+    }
+    __syncthreads();
+    // ---- chunk-fastest stream-out: lane = (chunk octet position, u); Y[row][u*(W/C) + cb*R + g]
+    const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
+    if (rb < a.M) {
+      double *yrow = Y + (int64_t)rb * a.Wout + (int64_t)cbk * a.R;
+      const int g_lo = lane & 7;
+      for (int w = warp; w < (nchunks / 8) * (C / 4); w += NW) {
+        const int oct = w / (C / 4), u0 = (w - oct * (C / 4)) * 4 + (lane >> 3);
+        const int g = oct * 8 + g_lo;
+        const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
+        const double v = *reinterpret_cast<const double *>(buf + (uint32_t)g * CB +
+                                                           (rowswz32((uint32_t)u0 / P, (uint32_t)u0 % P) ^ gx));
+        if ((int64_t)cbk * a.R + g < a.WC) yrow[(int64_t)u0 * a.WC + g] = v;
+      }
+    }
+    __syncthreads();  // the stage is fully consumed
+    if (tid == 0) issue_load(it + a.stages);
+  }
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
@@ -1096,6 +1249,8 @@ const FusedInstance kInstances[] = {
     {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
     // L2-fused pair of factor pipelines (two passes in one cooperative launch): id 29
     {KRON_F32, 8, 64, 8, 4, 2},
+    // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 256 * RS * P = 8 chunks): id 30
+    {KRON_F64, 32, 256, 1, 5, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1105,6 +1260,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
+    case 30: return kron_fused_dmma2_kernel<8>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -1288,7 +1444,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.M = M;
   size_t smem;
   int threads = inst.NT;
-  if (inst.warp == 3) {
+  if (inst.warp == 3 || inst.warp == 5) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
   } else if (inst.warp == 2 || inst.warp == 4) {
     smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
@@ -1297,7 +1453,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
   }
-  if (inst.warp == 3) {
+  if (inst.warp == 3 || inst.warp == 5) {
     Kernel4Fn k4 = instance_kernel4(pp.variant);
     const int slots = kernel_slots((const void *)k4, threads, smem);
     if (slots < 1) return (int)cudaErrorInvalidConfiguration;

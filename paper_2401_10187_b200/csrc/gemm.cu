@@ -209,12 +209,6 @@ int gemm_pick(int dtype, int Q) {
 // (3-D boxes {16, 2, rows} with the 128B swizzle: the two 128-byte lines of a row get different XOR
 // patterns, which makes both fragment gathers bank-conflict free); the epilogue writes C fragments
 // straight to Y[m, q*S + s] (8 consecutive slices = 64 bytes per column).
-__device__ __forceinline__ void dmma_m16n8k4(double (&c)[4], double a0, double a1, double b0) {
-  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
-               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
-               : "d"(a0), "d"(a1), "d"(b0));
-}
-
 template <int NWARP, int NS>
 __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __grid_constant__ CUtensorMap tm_a,
                                                                        const __grid_constant__ CUtensorMap tm_b,

@@ -23,9 +23,9 @@ timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron
    python bench.py --config C32 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 4 -c 1 -o $OUT/prof_C64 \
    python bench.py --config C64 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_gemm -s 6 -c 1 -o $OUT/prof_D1 \
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_ -s 6 -c 1 -o $OUT/prof_D1 \
    python bench.py --config D1 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_gemm -s 6 -c 1 -o $OUT/prof_D2 \
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_ -s 6 -c 1 -o $OUT/prof_D2 \
    python bench.py --config D2 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 6 -c 2 -o $OUT/prof_E \
    python bench.py --config E --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
