@@ -56,9 +56,13 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   if (tileM > 1 && lines > 256) return false;
   if (C > 256 && (C % 256 || C / 256 > 256)) return false;
   if (inst.warp && ((int64_t)32 * inst.rsw * p) % C) return false;  // warp share = whole chunks
-  if (inst.warp == 3 || inst.warp == 5) {
+  if (inst.warp == 3) {
     // two-factor chunk GEMMs: exactly two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
+  }
+  if (inst.warp == 5) {
+    // DMMA chunk pairs: exactly two factors, one tile row of 4 chunks (32-byte fp64 runs)
+    if (k != 2 || tileM != 1 || R != 4 || (R * C) != E) return false;
   }
   if (inst.warp == 2 || inst.warp == 4) {
     if (k > 3) return false;                                   // one warp group per factor
@@ -67,7 +71,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 3 || inst.warp == 5) {
+  if (inst.warp == 5) {
+    stages = 2;  // two CTAs per SM overlap one another's stream-out phase
+  } else if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
   } else if (inst.warp == 4) {
     if (tileM != 1) return false;

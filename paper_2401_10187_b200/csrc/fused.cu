@@ -1086,8 +1086,8 @@ __device__ __forceinline__ uint32_t rowswz32(uint32_t r, uint32_t c) {  // [rows
   return line * 128u + (((c & 15u) << 3) ^ ((line & 7u) << 4));
 }
 
-template <int NW>
-__global__ void __launch_bounds__(NW * 32, 1) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
+template <int NW, int RC>
+__global__ void __launch_bounds__(NW * 32, 2) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                      const FusedArgs a) {
   constexpr int P = 32, C = P * P, LINE = 16;
   constexpr uint32_t CB = C * 8;  // chunk bytes
@@ -1211,10 +1211,12 @@ __global__ void __launch_bounds__(NW * 32, 1) kron_fused_dmma2_kernel(const __gr
     const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
     if (rb < a.M) {
       double *yrow = Y + (int64_t)rb * a.Wout + (int64_t)cbk * a.R;
-      const int g_lo = lane & 7;
-      for (int w = warp; w < (nchunks / 8) * (C / 4); w += NW) {
-        const int oct = w / (C / 4), u0 = (w - oct * (C / 4)) * 4 + (lane >> 3);
-        const int g = oct * 8 + g_lo;
+      // RC consecutive chunks per u: lanes (g_lo = lane % RC, u offset = lane / RC)
+      constexpr int UPW = 32 / RC;
+      const int g_lo = lane % RC;
+      for (int w = warp; w < (nchunks / RC) * (C / UPW); w += NW) {
+        const int oct = w / (C / UPW), u0 = (w - oct * (C / UPW)) * UPW + lane / RC;
+        const int g = oct * RC + g_lo;
         const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
         const double v = *reinterpret_cast<const double *>(buf + (uint32_t)g * CB +
                                                            (rowswz32((uint32_t)u0 / P, (uint32_t)u0 % P) ^ gx));
@@ -1249,8 +1251,8 @@ const FusedInstance kInstances[] = {
     {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
     // L2-fused pair of factor pipelines (two passes in one cooperative launch): id 29
     {KRON_F32, 8, 64, 8, 4, 2},
-    // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 256 * RS * P = 8 chunks): id 30
-    {KRON_F64, 32, 256, 1, 5, 0},
+    // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 128 * RS * P = 4 chunks): id 30
+    {KRON_F64, 32, 128, 1, 5, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1260,7 +1262,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
-    case 30: return kron_fused_dmma2_kernel<8>;
+    case 30: return kron_fused_dmma2_kernel<4, 4>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
