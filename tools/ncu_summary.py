@@ -76,6 +76,7 @@ def main():
     for d in s:
         name = d["kernel"]
         key = ("kron_fused_kernel" if "kron_fused" in name else "kron_gemm_kernel" if "kron_gemm" in name
+               else "kron_dmma_kernel" if "kron_dmma" in name
                else "sliced_generic_kernel" if "sliced_generic" in name else None)
         if key and "dram_bytes" in d:
             traffic.setdefault(cfg, {})[key] = int(d["dram_bytes"])
