@@ -464,7 +464,8 @@ def main():
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
                 "frac": round(ach / alu_peak, 4),
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")}
-    kname = {"fused": "kron_fused_kernel", "generic": "sliced_generic_kernel", "gemm": "kron_gemm"}[kind]
+    kname = {"fused": "kron_fused_kernel", "generic": "sliced_generic_kernel",
+             "gemm": "kron_dmma_kernel" if es == 8 else "kron_gemm_kernel"}[kind]
     roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
                  "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
                  "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
