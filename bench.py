@@ -358,6 +358,8 @@ def main():
                     help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
                          "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
     ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
+    ap.add_argument("--autotune", action=argparse.BooleanOptionalAction, default=True,
+                    help="autotune the pass plan before warm-up (P:599-619); --no-autotune = static plan")
     ap.add_argument("--sweep", default=None, choices=["table3", "table4"],
                     help="paper shape sweeps (one JSON line per shape) instead of the headline bench")
     args = ap.parse_args()
@@ -403,6 +405,11 @@ def main():
     Fs_h = synth.factors(P, Q, seed, "urand", dt)
     Fs = [torch.from_numpy(f).to(dev) for f in Fs_h]
     Y = torch.empty((M, L), dtype=tdt, device=dev)
+    tuned = None
+    if args.autotune:
+        # time the candidate plans on these buffers, keep the fastest (untimed, before warm-up)
+        _, ncand, best = kron.autotune(X, Fs, Y, reps=3)
+        tuned = {"candidates": ncand, "best_ms": round(best, 5)}
     wsz = kron.workspace_size(M, P, Q, tdt)
     work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
     plan = kron.plan_describe(M, P, Q, tdt)
@@ -530,7 +537,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
             "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
             "config": {"workload": args.config, "M_per_gpu": M, "P": P, "Q": Q, "K": K, "L": L,
-                       "plan": [list(p) for p in plan],
+                       "plan": [list(p) for p in plan], "autotune": tuned,
                        "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,

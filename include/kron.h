@@ -92,6 +92,24 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
                                  kron_dtype_t dtype, int32_t cap, int32_t *npasses, int32_t *first,
                                  int32_t *nfactors, int32_t *kind);
 
+/* Autotuning ("performs auto-tuning over a range of tile size parameter values for the
+ * given shape ... find the kernel with the least execution time").  Candidate plans (fusion group
+ * caps x kernel-family choices x fp64 DMMA on/off; duplicates removed) are each run once untimed and
+ * `reps` times between CUDA events on `stream` with the caller's X, F and Y (Y receives the correct
+ * result); the fastest is installed in the plan cache for (device, M, shapes, dtype), so subsequent
+ * kron_matmul / kron_matmul_ws calls use it.  Synchronous (waits for `stream`).  *ncand receives the
+ * number of distinct candidates and *best_ms the winner's mean time (both optional).              */
+kron_status_t kron_autotune(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                            const void *const *F, void *Y, kron_dtype_t dtype, int32_t reps, void *stream,
+                            int32_t *ncand, float *best_ms);
+
+/* Number of distinct candidate plans kron_autotune would time for this problem (host only). */
+kron_status_t kron_autotune_candidates(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                       int32_t *ncand);
+
+/* Drop every cached (static or autotuned) plan. */
+kron_status_t kron_plan_cache_clear(void);
+
 /* Algorithmic HBM bytes and FLOPs of the plan:
  *   bytes = sum_passes s*M*(W_in + W_out) + sum_f s*P_f*Q_f,   flops = sum_f 2*M*W_f*Q_f.      */
 kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -230,7 +231,8 @@ kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int
   return KRON_OK;
 }
 
-kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan, int64_t lead) {
+kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan, int64_t lead,
+                        const PlanPolicy &policy) {
   kron_status_t st = validate(M, N, P, Q, dtype);
   if (st != KRON_OK) return st;
   if (lead < 1) return KRON_ERR_INVALID_ARG;
@@ -252,11 +254,13 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
   while (f >= 1) {
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
-    const int inst_d = (p == q && !getenv("KRON_NO_DMMA")) ? fused_find(dtype, p, 5) : -1;
-    const int inst_g = (p == q) ? fused_find(dtype, p, 3) : -1;
-    const int inst_p = (p == q) ? fused_find(dtype, p, 2) : -1;
-    const int inst_w = (p == q) ? fused_find(dtype, p, 1) : -1;
-    const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;
+    const bool dmma_ok = policy.dmma && !getenv("KRON_NO_DMMA");
+    auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
+    const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
+    const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
+    const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
+    const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;
+    const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;  // always allowed: any chunk size
     if (inst_c >= 0) {
       int run = 1;  // consecutive factors of the same square shape
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
@@ -271,7 +275,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       };
       int kmax = 0;
       PassPlan probe;
-      for (int k = 1; k <= run && k <= kMaxFused; ++k)
+      for (int k = 1; k <= run && k <= kMaxFused && k <= policy.kcap; ++k)
         if (pick(k, &probe) >= 0) kmax = k;
       if (kmax >= 1) {
         // fewest passes, then balanced group sizes ("ceil(N/Fused) iterations")
@@ -300,6 +304,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     pp.W_in = W;
     pp.W_out = plan->W[f - 1];
     pp.kind = gemm_supported(dtype, Mp, W, p, q) ? KIND_GEMM : KIND_GENERIC;
+    pp.variant = (pp.kind == KIND_GEMM && dtype == KRON_F64 && policy.dmma && p % 16 == 0 && q % 16 == 0) ? 1 : 0;
     plan->passes.push_back(pp);
     f -= 1;
   }
@@ -452,12 +457,121 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
   return st;
 }
 
+// Candidate plans for the autotuner: fusion-depth caps x kernel-family masks x fp64 DMMA,
+// duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
+std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
+  // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
+  const unsigned all = 0x3Fu;
+  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 3) | (1u << 5)), (1u << 0) | (1u << 1)};
+  const int caps[] = {kMaxFused, 3, 2, 1};
+  std::vector<Plan> cands;
+  auto same = [](const Plan &a, const Plan &b) {
+    if (a.passes.size() != b.passes.size()) return false;
+    for (size_t i = 0; i < a.passes.size(); ++i) {
+      const PassPlan &x = a.passes[i], &y = b.passes[i];
+      if (x.kind != y.kind || x.variant != y.variant || x.first != y.first || x.nf != y.nf || x.tileK != y.tileK ||
+          x.tileM != y.tileM || x.stages != y.stages)
+        return false;
+    }
+    return true;
+  };
+  for (int dm = 1; dm >= 0; --dm)
+    for (unsigned km : kinds)
+      for (int cap : caps) {
+        PlanPolicy pol;
+        pol.kcap = cap;
+        pol.kinds = km;
+        pol.dmma = dm == 1;
+        Plan pl;
+        if (make_plan(M, N, P, Q, dtype, &pl, 1, pol) != KRON_OK) continue;
+        bool dup = false;
+        for (const Plan &c : cands) dup |= same(c, pl);
+        if (!dup) cands.push_back(pl);
+      }
+  return cands;
+}
+
+kron_status_t kron_autotune_candidates(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                       int32_t *ncand) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (!ncand) return KRON_ERR_INVALID_ARG;
+  *ncand = M == 0 ? 0 : (int32_t)autotune_candidates(M, N, P, Q, (int)dtype).size();
+  return KRON_OK;
+}
+
+kron_status_t kron_plan_cache_clear(void) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.clear();
+  return KRON_OK;
+}
+
+kron_status_t kron_autotune(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                            const void *const *F, void *Y, kron_dtype_t dtype, int32_t reps, void *stream,
+                            int32_t *ncand, float *best_ms) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X || !F || !Y || reps < 1) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  std::vector<Plan> cands = autotune_candidates(M, N, P, Q, (int)dtype);
+  if (cands.empty()) return KRON_ERR_UNSUPPORTED;
+  size_t wsmax = 0;
+  for (const Plan &c : cands) wsmax = std::max(wsmax, ws_bytes_of(c));
+  cudaStream_t s = (cudaStream_t)stream;
+  void *ws = nullptr;
+  keep_pool_cached();
+  if (wsmax && cudaMallocAsync(&ws, wsmax, s) != cudaSuccess) {
+    cudaGetLastError();
+    return KRON_ERR_NO_MEMORY;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int best = -1;
+  float best_t = 0.f;
+  for (size_t i = 0; i < cands.size() && st == KRON_OK; ++i) {
+    st = run_plan(cands[i], X, F, Y, ws, stream);  // warm-up (also primes kernel attributes)
+    if (st != KRON_OK) break;
+    cudaEventRecord(e0, s);
+    for (int r = 0; r < reps && st == KRON_OK; ++r) st = run_plan(cands[i], X, F, Y, ws, stream);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) st = cuda_fail((int)cudaGetLastError(), "autotune timing");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= (float)reps;
+    if (st == KRON_OK && (best < 0 || ms < best_t)) {
+      best = (int)i;
+      best_t = ms;
+    }
+  }
+  // leave Y holding the result of the chosen plan
+  if (st == KRON_OK) st = run_plan(cands[best], X, F, Y, ws, stream);
+  if (ws) cudaFreeAsync(ws, s);
+  cudaStreamSynchronize(s);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != KRON_OK) return st;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  PlanKey key{dev, M, (int)dtype, std::vector<int32_t>(P, P + N), std::vector<int32_t>(Q, Q + N)};
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache[key] = std::make_shared<Plan>(cands[best]);
+  }
+  if (ncand) *ncand = (int32_t)cands.size();
+  if (best_ms) *best_ms = best_t;
+  return KRON_OK;
+}
+
 kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
                                  int32_t cap, int32_t *npasses, int32_t *first, int32_t *nfactors, int32_t *kind) {
   if (!npasses) return KRON_ERR_INVALID_ARG;
-  Plan plan;
-  kron_status_t st = make_plan(M, N, P, Q, (int)dtype, &plan);
+  std::shared_ptr<const Plan> pl;
+  kron_status_t st = cached_plan(M, N, P, Q, (int)dtype, &pl);
   if (st != KRON_OK) return st;
+  const Plan &plan = *pl;
   *npasses = (int32_t)plan.passes.size();
   for (int i = 0; i < (int)plan.passes.size() && i < cap; ++i) {
     if (first) first[i] = plan.passes[i].first;
@@ -469,9 +583,10 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
 
 kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
                              double *hbm_bytes, double *flops) {
-  Plan plan;
-  kron_status_t st = make_plan(M, N, P, Q, (int)dtype, &plan);
+  std::shared_ptr<const Plan> pl;
+  kron_status_t st = cached_plan(M, N, P, Q, (int)dtype, &pl);
   if (st != KRON_OK) return st;
+  const Plan &plan = *pl;
   const double es = es_of((int)dtype);
   double b = 0, fl = 0;
   for (const PassPlan &pp : plan.passes) b += es * (double)M * (double)(pp.W_in + pp.W_out);

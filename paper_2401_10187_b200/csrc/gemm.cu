@@ -392,7 +392,7 @@ bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q) {
 }
 
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream) {
-  if (dtype == KRON_F64 && pp.P % 16 == 0 && pp.Q % 16 == 0 && !getenv("KRON_NO_DMMA"))
+  if (dtype == KRON_F64 && pp.variant == 1 && pp.P % 16 == 0 && pp.Q % 16 == 0 && !getenv("KRON_NO_DMMA"))
     return launch_dmma(pp, M, in, out, F, stream);
   const int es = dtype == KRON_F32 ? 4 : 8;
   const int gi = gemm_pick(dtype, pp.Q);

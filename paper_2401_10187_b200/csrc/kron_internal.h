@@ -47,8 +47,15 @@ struct Plan {
 };
 
 // Builds the plan (host only).  Returns KRON_OK or a validation error.
+// Knobs the autotuner searches over; the default policy is the static planner.
+struct PlanPolicy {
+  int kcap = kMaxFused;       // largest fused group
+  unsigned kinds = 0x3Fu;     // allowed fused kernel families (bit = FusedInstance::warp)
+  bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
+  bool operator==(const PlanPolicy &o) const { return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma; }
+};
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
-                        int64_t lead = 1);
+                        int64_t lead = 1, const PlanPolicy &policy = PlanPolicy());
 size_t plan_ws_bytes(const Plan &plan);
 void keep_pool_cached();  // default mem pool keeps freed blocks (stream-ordered workspaces)
 // Enqueue every pass of `plan` (F indexed like the plan's P/Q arrays); ws >= plan_ws_bytes bytes.

@@ -50,6 +50,14 @@ _lib.kron_dist_plan.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ct
 _lib.kron_dist_grid_rule.restype = ctypes.c_int
 _lib.kron_dist_grid_rule.argtypes = [ctypes.c_int32, _i32p, _i32p]
 
+_lib.kron_autotune.restype = ctypes.c_int
+_lib.kron_autotune.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
+                               ctypes.c_int, ctypes.c_int32, ctypes.c_void_p, _i32p, ctypes.POINTER(ctypes.c_float)]
+_lib.kron_autotune_candidates.restype = ctypes.c_int
+_lib.kron_autotune_candidates.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, _i32p]
+_lib.kron_plan_cache_clear.restype = ctypes.c_int
+_lib.kron_plan_cache_clear.argtypes = []
+
 KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm"}
 
 
@@ -192,6 +200,36 @@ def matmul_ws_events(X, Fs, out, workspace, events, stream=None):
                                       dtype_code(X.dtype), wptr, wbytes, Ev, len(events), _stream_ptr(stream)),
            "kron_matmul_ws_events")
     return out
+
+
+def autotune(X, Fs, out=None, reps: int = 3, stream=None):
+    """kron_autotune(): time every candidate plan on these buffers, install the fastest for this
+    (device, M, shapes, dtype).  Returns (Y, number of candidates, best ms)."""
+    import torch
+    P, Q = _prep(X, Fs)
+    L = 1
+    for q in Q:
+        L *= q
+    if out is None:
+        out = torch.empty((X.shape[0], L), dtype=X.dtype, device=X.device)
+    Pa, Qa = _shape_arrays(P, Q)
+    Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
+    n, ms = ctypes.c_int32(), ctypes.c_float()
+    _check(_lib.kron_autotune(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype),
+                              reps, _stream_ptr(stream), ctypes.byref(n), ctypes.byref(ms)), "kron_autotune")
+    return out, n.value, ms.value
+
+
+def autotune_candidates(M: int, P, Q, dtype) -> int:
+    Pa, Qa = _shape_arrays(P, Q)
+    n = ctypes.c_int32()
+    _check(_lib.kron_autotune_candidates(M, len(P), Pa, Qa, dtype_code(dtype), ctypes.byref(n)),
+           "kron_autotune_candidates")
+    return n.value
+
+
+def plan_cache_clear() -> None:
+    _check(_lib.kron_plan_cache_clear(), "kron_plan_cache_clear")
 
 
 def raw_lib():

@@ -152,3 +152,15 @@ def test_dist_plan_paper_local(kron):
     assert len(rounds) == 2 and sorted(rounds) == [2, 3]
     with pytest.raises(kron.KronError):
         kron.dist_plan(4095, [16] * 5, [16] * 5, 4, 2)  # GM does not divide M
+
+
+def test_autotune_candidates(kron):
+    # the autotuner times alternative plans; the static plan is always one of them
+    assert kron.autotune_candidates(1024, [8] * 6, [8] * 6, "float32") >= 3   # fusion caps 3/2/1 + families
+    assert kron.autotune_candidates(1024, [32] * 4, [32] * 4, "float64") >= 2  # + DMMA on/off
+    assert kron.autotune_candidates(16, [4, 4], [4, 4], "float32") == 1       # generic only
+    assert kron.autotune_candidates(0, [8] * 2, [8] * 2, "float32") == 0
+    lib = kron.raw_lib()
+    Pa = (ctypes.c_int32 * 2)(2, 2)
+    assert lib.kron_autotune(4, 2, Pa, Pa, None, None, None, 0, 3, None, None, None) == 1  # null buffers
+    assert lib.kron_plan_cache_clear() == 0

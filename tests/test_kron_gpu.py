@@ -188,3 +188,23 @@ def test_full_size_sampled_rows(kron, cuda_device, name, cfg, M, P, Q, dt):
     torch.cuda.empty_cache()
     ref = oracle.alg1(synth.rows_of(rows, K, seed, 0, "urand"), Fs_h)
     assert rel_err(Ys, ref) <= TOL[dt]
+
+
+@pytest.mark.parametrize("M,P,Q,dt", [
+    (40, [8] * 6, [8] * 6, np.float32),
+    (24, [32] * 4, [32] * 4, np.float64),
+    (20, [16] * 5, [16] * 5, np.float32),
+    (9, [64] * 3, [32] * 3, np.float64),
+])
+def test_autotuned_plan_parity(kron, cuda_device, M, P, Q, dt):
+    # the autotuner times every candidate on the caller's buffers and installs the
+    # fastest; its output and every later call through the installed plan stay bit-exact
+    mode = "int1" if dt == np.float32 else "int"
+    X, Fs = case(M, P, Q, dt, mode, 7)
+    ref = oracle.alg1(X, Fs).astype(dt)
+    Xd, Fd = to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs]
+    Y, n, ms = kron.autotune(Xd, Fd, reps=2)
+    assert n >= 1 and ms > 0
+    assert np.array_equal(Y.cpu().numpy(), ref)
+    assert np.array_equal(run(kron, X, Fs, cuda_device), ref)
+    kron.plan_cache_clear()
