@@ -9,7 +9,7 @@ if [ "${TESTS:-1}" = "1" ]; then
 fi
 for c in "$@"; do
   timeout 300 python bench.py --config $c --steps ${STEPS:-50} --warmup 5 --no-cpu --no-e2e > $OUT/bench_$c.json 2> $OUT/bench_$c.err
-  python -c "import json,sys; d=json.load(open('$OUT/bench_$c.json')); r=d['roofline']; print('$c', d['value'], 'GF/s', d['ms_per_step'],'ms', r['bound'], r['achieved'], r['unit'], 'frac', r['frac'], 'step_frac', d['step_roofline']['frac'], d['clocks'])" || tail -5 $OUT/bench_$c.err
+  python -c "import json,sys; d=json.load(open('$OUT/bench_$c.json')); r=d['roofline']; print('$c', d['value'], 'GF/s', d['ms_per_step'],'ms', r['bound'], r['achieved'], r['unit'], 'frac', r['frac'], 'step_frac', d['step_roofline']['frac'], d['config'].get('plan'), d['config'].get('autotune'), d['clocks'].get('sm_mhz'))" || tail -5 $OUT/bench_$c.err
 done
 if [ -n "${NCU_CFG:-}" ]; then
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:${NCU_K:-kron_} -s ${NCU_S:-6} -c 1 -o $OUT/prof_$NCU_CFG \
