@@ -60,6 +60,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   if (inst.warp == 3) {
     // two-factor chunk GEMMs: exactly two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
+    if (W * es >= (int64_t(1) << 32)) return false;  // 32-bit in-row store offsets
   }
   if (inst.warp == 5) {
     // DMMA chunk pairs: exactly two factors, one tile row of 4 chunks (32-byte fp64 runs)

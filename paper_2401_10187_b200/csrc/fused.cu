@@ -1013,6 +1013,48 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
       // Z row s, columns q1base..q1base+RN: a 32/64-byte aligned block inside one 128-byte line
       const uint32_t zb0 = gg * C * ES + (uint32_t)q1base * ES;
       T acc[RM][RN];
+      if constexpr (ES == 4 && (P == 16 || P == 32)) {
+        // fp32: the row-s / granule-h address is  gg*C*4 + line(s)*128 + (K ^ (v(s,h) << 4)), with
+        // K = q1base*4 ^ gx a lane constant and v a compile-time 3-bit value (the 128B-swizzle line bits,
+        // the half-line bit of 64-byte rows and h are disjoint), so eight per-unit offsets o[v] turn every
+        // Z load into [register + immediate].
+        constexpr int PE = P * ES;
+        const uint32_t K = ((uint32_t)q1base * ES) ^ gx;
+        const T *fr0 = F2 + q2base;
+#pragma unroll 1
+        for (int s0 = 0; s0 < P; s0 += 8) {
+          // rows s0..s0+7: line(s) = line(s0) + line(s'), and the swizzle bits of line(s0) (0 or 4) XOR
+          // into those of line(s') without carry, so one lane constant per block absorbs them
+          const int line0 = (s0 * PE) >> 7;
+          const uint32_t Kb = K ^ ((uint32_t)(line0 & 7) << 4);
+          const uint32_t b0 = gg * C * ES + (uint32_t)line0 * 128;
+#pragma unroll
+          for (int sp = 0; sp < 8; ++sp) {
+            const int line = (sp * PE) >> 7, a4 = ((sp * PE) & 127) >> 4;
+            const float4 fv4 = *reinterpret_cast<const float4 *>(fr0 + (s0 + sp) * P);
+            const float fv[4] = {fv4.x, fv4.y, fv4.z, fv4.w};
+            float zv[8];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t v = (uint32_t)(a4 ^ h ^ (line & 7));
+              const float4 t = *reinterpret_cast<const float4 *>(buf + b0 + (Kb ^ (v << 4)) + line * 128);
+              zv[4 * h] = t.x; zv[4 * h + 1] = t.y; zv[4 * h + 2] = t.z; zv[4 * h + 3] = t.w;
+            }
+            const bool first = s0 == 0 && sp == 0;
+#pragma unroll
+            for (int i = 0; i < RM; ++i) {
+#pragma unroll
+              for (int j = 0; j < RN; j += 2) {
+                const float2 zz = make_float2(zv[j], zv[j + 1]);
+                const float2 r2 = first ? __fmul2_rn(make_float2(fv[i], fv[i]), zz)
+                                        : __ffma2_rn(make_float2(fv[i], fv[i]), zz, make_float2(acc[i][j], acc[i][j + 1]));
+                acc[i][j] = r2.x;
+                acc[i][j + 1] = r2.y;
+              }
+            }
+          }
+        }
+      } else {
 #pragma unroll 4
       for (int s = 0; s < P; ++s) {
         T fv[RM], zv[RN];
@@ -1056,16 +1098,19 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
           }
         }
       }
+      }
       // direct-index store: u = q2*P + q1 -> Y[row][u*(W/C) + cb*R + g]
       const int64_t gcol = (int64_t)cb * a.R + gg;
       if (gcol < a.WC && rb < a.M) {
         T *yb = Y + (int64_t)rb * a.Wout + gcol + (int64_t)(q2base * P + q1base) * a.WC;
+        // every output of the unit sits (i*P + j) * WC elements past yb (< 2^32 bytes: one row of Y)
+        const uint32_t wcb = (uint32_t)a.WC * (uint32_t)ES;
 #pragma unroll
-        for (int i = 0; i < RM; ++i) {
-          T *yi = yb + (int64_t)(i * P) * a.WC;
+        for (int i = 0; i < RM; ++i)
 #pragma unroll
-          for (int j = 0; j < RN; ++j) yi[(int64_t)j * a.WC] = acc[i][j];
-        }
+          for (int j = 0; j < RN; ++j)
+            *reinterpret_cast<T *>(reinterpret_cast<unsigned char *>(yb) + (uint64_t)(wcb * (uint32_t)(i * P + j))) =
+                acc[i][j];
       }
     }
     __syncthreads();  // the stage is fully consumed
