@@ -74,7 +74,8 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
   if (inst.warp == 5) {
-    stages = 2;  // two CTAs per SM overlap one another's stream-out phase
+    stages = (int)((220 * 1024 - 2 * (int64_t)p * p * es) / stage);  // one warp-specialised CTA per SM
+    if (stages > 8) stages = 8;
   } else if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
   } else if (inst.warp == 4) {

@@ -22,6 +22,7 @@
 // TB/s for 16-byte runs against ~5 TB/s for >= 32-byte runs, so the planner keeps R*s >= 32.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include <map>
@@ -1131,60 +1132,68 @@ __device__ __forceinline__ uint32_t rowswz32(uint32_t r, uint32_t c) {  // [rows
   return line * 128u + (((c & 15u) << 3) ^ ((line & 7u) << 4));
 }
 
-template <int NW, int RC>
-__global__ void __launch_bounds__(NW * 32, 2) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
-                                                                     const FusedArgs a) {
-  constexpr int P = 32, C = P * P, LINE = 16;
+// Warp-specialised: NCW compute warps (one chunk each; with NCW = 2 * CPT two groups take alternate
+// tiles so every SM sub-partition has two DMMA warps) never stop for the HBM stream-out, which NSW
+// store warps do from the finished tile while the compute warps work on the next ones (mbarriers:
+// full = TMA landed, cdone = chunks computed, empty = tile streamed out -> refill).
+template <int NCW, int NSW>
+__global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                             const FusedArgs a) {
+  constexpr int P = 32, C = P * P, LINE = 16, CPT = 4;  // chunks per tile
+  static_assert(NCW % CPT == 0, "compute warps come in groups of one tile");
   constexpr uint32_t CB = C * 8;  // chunk bytes
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char *F1s = base + (size_t)a.stages * a.stage_bytes;  // [p][q1]
   unsigned char *F2Ts = F1s + CB;                                 // [q2][s] = F2[s][q2]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(F2Ts + CB);
+  uint64_t *full = reinterpret_cast<uint64_t *>(F2Ts + CB);
+  uint64_t *cdone = full + a.stages, *empty = cdone + a.stages;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gq = lane >> 2, tq = lane & 3;
 
   {
     const double *F1 = reinterpret_cast<const double *>(a.F[0]);
     const double *F2 = reinterpret_cast<const double *>(a.F[1]);
-    for (int i = tid; i < C; i += NW * 32) {
+    for (int i = tid; i < C; i += (NCW + NSW) * 32) {
       const uint32_t r = (uint32_t)i / P, c = (uint32_t)i % P;
       *reinterpret_cast<double *>(F1s + rowswz32(r, c)) = F1[i];   // F1[p = r][q1 = c]
       *reinterpret_cast<double *>(F2Ts + rowswz32(c, r)) = F2[i];  // F2[s = r][q2 = c] -> F2T[c][r]
     }
   }
   if (tid == 0) {
-    for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], CPT);
+      mbar_init(&empty[s], NSW);
+    }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
   }
   __syncthreads();
-  const int nchunks = a.R;  // tileM == 1
   auto issue_load = [&](int it) {
     const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
     if (tile >= a.ntiles) return;
     const int st = it % a.stages;
     const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
     unsigned char *dst = base + (size_t)st * a.stage_bytes;
-    mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
+    mbar_arrive_expect_tx(&full[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb);
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
-  double *Y = reinterpret_cast<double *>(a.Y);
 
-  for (int it = 0;; ++it) {
-    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
-    if (tile >= a.ntiles) break;
-    const int st = it % a.stages;
-    mbar_wait(&bars[st], (uint32_t)((it / a.stages) & 1));
-    unsigned char *buf = base + (size_t)st * a.stage_bytes;
-
-    for (int g = warp; g < nchunks; g += NW) {
-      unsigned char *cb0 = buf + (uint32_t)g * CB;
-      const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
+  if (warp < NCW) {
+    // ---------------- compute warps: chunk (warp % CPT) of every (NCW / CPT)-th tile
+    const int g = warp % CPT;
+    const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
+    for (int it = warp / CPT;; it += NCW / CPT) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
+      unsigned char *cb0 = base + (size_t)st * a.stage_bytes + (uint32_t)g * CB;
       double acc[2][4][4];
       // ---- GEMM1: Z[s][q1] = sum_p X[s][p] F1[p][q1]
 #pragma unroll
@@ -1250,26 +1259,43 @@ __global__ void __launch_bounds__(NW * 32, 2) kron_fused_dmma2_kernel(const __gr
             *reinterpret_cast<double2 *>(cb0 + (rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
                 make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
       __syncwarp();
+      if (lane == 0) mbar_arrive(&cdone[st]);
     }
-    __syncthreads();
-    // ---- chunk-fastest stream-out: lane = (chunk octet position, u); Y[row][u*(W/C) + cb*R + g]
-    const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
-    if (rb < a.M) {
-      double *yrow = Y + (int64_t)rb * a.Wout + (int64_t)cbk * a.R;
-      // RC consecutive chunks per u: lanes (g_lo = lane % RC, u offset = lane / RC)
-      constexpr int UPW = 32 / RC;
-      const int g_lo = lane % RC;
-      for (int w = warp; w < (nchunks / RC) * (C / UPW); w += NW) {
-        const int oct = w / (C / UPW), u0 = (w - oct * (C / UPW)) * UPW + lane / RC;
-        const int g = oct * RC + g_lo;
-        const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
-        const double v = *reinterpret_cast<const double *>(buf + (uint32_t)g * CB +
-                                                           (rowswz32((uint32_t)u0 / P, (uint32_t)u0 % P) ^ gx));
-        if ((int64_t)cbk * a.R + g < a.WC) yrow[(int64_t)u0 * a.WC + g] = v;
+  } else {
+    // ---------------- store warps: chunk-fastest stream-out, Y[row][u*(W/C) + cb*R + g]
+    const int sw = warp - NCW;
+    double *Y = reinterpret_cast<double *>(a.Y);
+    constexpr int UPW = 32 / CPT;  // u values per warp instruction (CPT consecutive chunks each)
+    const int g = lane % CPT;
+    const uint32_t gx = pipe_gx<8, 4>((uint32_t)g);
+    for (int it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      const uint32_t par = (uint32_t)((it / a.stages) & 1);
+      mbar_wait(&cdone[st], par);
+      const unsigned char *buf = base + (size_t)st * a.stage_bytes + (uint32_t)g * CB;
+      const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
+      if (rb < a.M && (int64_t)cbk * a.R + g < a.WC) {
+        double *yg = Y + (int64_t)rb * a.Wout + (int64_t)cbk * a.R + g;
+#pragma unroll 4
+        for (int w = sw; w < C / UPW; w += NSW) {
+          const int u = w * UPW + lane / CPT;
+          const double v = *reinterpret_cast<const double *>(buf + (rowswz32((uint32_t)u / P, (uint32_t)u % P) ^ gx));
+          yg[(int64_t)u * a.WC] = v;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (sw == 0) {
+        if (lane == 0) {
+          mbar_wait(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + a.stages);
+        }
+        __syncwarp();
       }
     }
-    __syncthreads();  // the stage is fully consumed
-    if (tid == 0) issue_load(it + a.stages);
   }
 }
 
@@ -1307,7 +1333,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
-    case 30: return kron_fused_dmma2_kernel<4, 4>;
+    case 30: return kron_fused_dmma2_kernel<8, 4>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -1491,7 +1517,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.M = M;
   size_t smem;
   int threads = inst.NT;
-  if (inst.warp == 3 || inst.warp == 5) {
+  if (inst.warp == 5) {
+    smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
+    threads = 32 * (8 + 4);  // kron_fused_dmma2_kernel<8, 4>
+  } else if (inst.warp == 3) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
   } else if (inst.warp == 2 || inst.warp == 4) {
     smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
