@@ -62,6 +62,10 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
     if (W * es >= (int64_t(1) << 32)) return false;  // 32-bit in-row store offsets
   }
+  if (inst.warp == 6) {
+    // warp-specialised fp32 chunk pairs: two factors, one tile row of whole chunk octets
+    if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
+  }
   if (inst.warp == 5) {
     // DMMA chunk pairs: exactly two factors, one tile row of 4 chunks (32-byte fp64 runs)
     if (k != 2 || tileM != 1 || R != 4 || (R * C) != E) return false;
@@ -73,8 +77,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 5) {
-    stages = (int)((220 * 1024 - 2 * (int64_t)p * p * es) / stage);  // one warp-specialised CTA per SM
+  if (inst.warp == 5 || inst.warp == 6) {
+    // one warp-specialised CTA per SM
+    stages = (int)((220 * 1024 - 2 * (int64_t)p * p * es) / stage);
     if (stages > 8) stages = 8;
   } else if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
@@ -259,6 +264,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const bool dmma_ok = policy.dmma && !getenv("KRON_NO_DMMA");
     auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
+    const int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;
@@ -269,6 +275,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
         if (inst_d >= 0 && fused_geometry(fused_instance(inst_d), k, W, Mp, pp)) return inst_d;
+        if (inst_s >= 0 && fused_geometry(fused_instance(inst_s), k, W, Mp, pp)) return inst_s;
         if (inst_g >= 0 && fused_geometry(fused_instance(inst_g), k, W, Mp, pp)) return inst_g;
         if (inst_p >= 0 && fused_geometry(fused_instance(inst_p), k, W, Mp, pp)) return inst_p;
         if (inst_w >= 0 && fused_geometry(fused_instance(inst_w), k, W, Mp, pp)) return inst_w;
@@ -463,8 +470,9 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x3Fu;
-  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 3) | (1u << 5)), (1u << 0) | (1u << 1)};
+  const unsigned all = 0x7Fu;
+  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 5) | (1u << 6)),
+                            all & ~((1u << 3) | (1u << 5) | (1u << 6)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
   std::vector<Plan> cands;
   auto same = [](const Plan &a, const Plan &b) {

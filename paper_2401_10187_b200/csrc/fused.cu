@@ -224,7 +224,6 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
     for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
     prefetch_tmap(&tm_in);
-    prefetch_tmap(&tm_out);
   }
 
   // Per-thread slice bookkeeping: identical for every tile (same tile geometry).
@@ -394,7 +393,6 @@ __global__ void __launch_bounds__(NT, MINB) kron_fused_warp_kernel(const __grid_
     for (int s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
     prefetch_tmap(&tm_in);
-    prefetch_tmap(&tm_out);
   }
 
   const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
@@ -1119,6 +1117,248 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
   }
 }
 
+// ------------------------------------------------------------------ fp32 two-factor chunks, warp-specialised (v6)
+//
+// The v4 sandwich OUT = F2^T . (X . F1) per P x P chunk (P = 16 / 32, fp32), with every chunk owned by
+// one warp from start to finish: GEMM1 (A = X rows from the TMA tile, B = F1) writes Z in place, GEMM2
+// (A = F2^T, B = Z) writes OUT in place, both with 4 x 8 register tiles of paired FFMA2 — no CTA barrier
+// on the compute side; work units (one warp's chunks) are dealt round-robin across tile boundaries.
+// Four store warps stream each finished tile out chunk-fastest (the direct-index store, P:325-329:
+// Y[row][u*(W/C) + g0 + g]) while the compute warps work on the next tiles of the TMA ring (mbarriers:
+// full = landed, cdone = computed, empty = streamed out -> refill).  Output runs are R*4 bytes; the
+// measured write rate of such runs (tools/microbench_scatter.cu: 2.9 TB/s at 32 B, 4.5 TB/s at 128 B,
+// profiles/r02_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
+template <int P, int NCW, int RM, int RN, int VA>
+__global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                              const __grid_constant__ CUtensorMap tm_out,
+                                                                              const FusedArgs a) {
+  using T = float;
+  constexpr int ES = 4, LINE = 32, C = P * P, PE = P * ES;
+  constexpr int NSW = 4;
+  constexpr int L1 = (P / RM) * (P / RN);  // lanes per chunk
+  constexpr int CPG = 32 / L1;             // chunks per warp (one work unit)
+  const int UPT = a.R / CPG;               // work units per tile
+  constexpr uint32_t CE = C * ES;          // chunk bytes (a multiple of 1024)
+  static_assert(L1 <= 32 && 32 % L1 == 0, "lane tiling");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  T *F1s = reinterpret_cast<T *>(base + (size_t)a.stages * a.stage_bytes);  // [p][q1], plain
+  unsigned char *F2Ts = reinterpret_cast<unsigned char *>(F1s + C);          // [q2][s], 128B-swizzled
+  uint64_t *full = reinterpret_cast<uint64_t *>(F2Ts + CE);
+  uint64_t *cdone = full + a.stages, *empty = cdone + a.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  {
+    const T *F1 = reinterpret_cast<const T *>(a.F[0]);
+    const T *F2 = reinterpret_cast<const T *>(a.F[1]);
+    for (int i = tid; i < C; i += (NCW + NSW) * 32) {
+      const uint32_t r = (uint32_t)i / P, c = (uint32_t)i % P;
+      F1s[i] = F1[i];
+      *reinterpret_cast<T *>(F2Ts + swz128(c * PE + r * ES)) = F2[i];  // F2[s = r][q2 = c] -> F2T[c][r]
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], UPT);
+      mbar_init(&empty[s], NSW);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * a.stage_bytes;
+    mbar_arrive_expect_tx(&full[st], a.tile_bytes);
+    const int line0 = cb * (a.tileK / LINE);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    const int c1 = lane / L1, tau = lane % L1;
+    const int sg = tau % (P / RM), q1g = tau / (P / RM);
+    // A-operand rows sg + (P/RM)*i of a 128B-swizzled [P][P] matrix at a 1024-aligned base
+    uint32_t arow[RM];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) arow[i] = swz128((uint32_t)(sg + (P / RM) * i) * PE);
+    // one warp-level P x P x P product: acc[i][j] = sum_k A[row_i][k] * B[k][q1g*RN + j], k in blocks of
+    // 8 (compile-time offsets inside a block; loadB(k0, kk, f) gets the block base and the offset)
+    auto gemm = [&](const unsigned char *A, auto loadB, T (&acc)[RM][RN]) {
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
+#pragma unroll 1
+      for (int k0 = 0; k0 < P; k0 += 8) {
+        uint32_t ab[RM];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) ab[i] = arow[i] ^ (uint32_t)(k0 * ES);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += VA) {
+          T xa[RM][VA];
+#pragma unroll
+          for (int i = 0; i < RM; ++i) {
+            if constexpr (VA == 4) {
+              const float4 v = *reinterpret_cast<const float4 *>(A + (ab[i] ^ (uint32_t)(kk * ES)));
+              xa[i][0] = v.x; xa[i][1] = v.y; xa[i][2] = v.z; xa[i][3] = v.w;
+            } else {
+              const float2 v = *reinterpret_cast<const float2 *>(A + (ab[i] ^ (uint32_t)(kk * ES)));
+              xa[i][0] = v.x; xa[i][1] = v.y;
+            }
+          }
+#pragma unroll
+          for (int e = 0; e < VA; ++e) {
+            T f[RN];
+            loadB(k0, kk + e, f);
+#pragma unroll
+            for (int i = 0; i < RM; ++i) {
+              const float2 xx = make_float2(xa[i][e], xa[i][e]);
+#pragma unroll
+              for (int j = 0; j < RN; j += 2) {
+                const float2 r2 = __ffma2_rn(xx, make_float2(f[j], f[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+                acc[i][j] = r2.x;
+                acc[i][j + 1] = r2.y;
+              }
+            }
+          }
+        }
+      }
+    };
+    // units are dealt round-robin over the compute warps across tile boundaries
+    for (int un = warp;; un += NCW) {
+      const int it = un / UPT, cg = un % UPT;
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
+      unsigned char *buf = base + (size_t)st * a.stage_bytes;
+      {
+        const uint32_t gg = (uint32_t)(cg * CPG + c1);
+        unsigned char *ch = buf + gg * CE;
+        const uint32_t gx = pipe_gx<8, 4>(gg);
+        T acc[RM][RN];
+        // GEMM1: Z = X . F1
+        gemm(ch, [&](int k0, int kk, T (&f)[RN]) {
+          const T *fr = F1s + (k0 + kk) * P + q1g * RN;
+#pragma unroll
+          for (int j = 0; j < RN; j += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(fr + j);
+            f[j] = v.x; f[j + 1] = v.y; f[j + 2] = v.z; f[j + 3] = v.w;
+          }
+        }, acc);
+        __syncwarp();
+        auto put = [&](uint32_t xr) {
+#pragma unroll
+          for (int i = 0; i < RM; ++i)
+#pragma unroll
+            for (int j = 0; j < RN; j += 4)
+              *reinterpret_cast<float4 *>(ch + ((arow[i] ^ (uint32_t)((q1g * RN + j) * ES)) ^ xr)) =
+                  make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        };
+        put(gx);  // Z (chunk-XOR'd: the chunks of one warp read Z rows in the same instruction)
+        __syncwarp();
+        // GEMM2: OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
+        // Z row k = k0 + kk: ch + line(k)*128 + (Kq ^ (v << 4)): the 128B-swizzle bits of line(k0) and
+        // line(kk) XOR without carry (k0 % 8 == 0), and the in-line bits of kk, j and q1g are disjoint
+        const uint32_t Kq = (uint32_t)(q1g * RN * ES) ^ gx;
+        gemm(F2Ts, [&](int k0, int kk, T (&f)[RN]) {
+          const int line0 = (k0 * PE) >> 7, line = (kk * PE) >> 7, a4 = ((kk * PE) & 127) >> 4;
+          const uint32_t Kb = Kq ^ ((uint32_t)(line0 & 7) << 4);
+          const unsigned char *zb = ch + (line0 + line) * 128;
+#pragma unroll
+          for (int j = 0; j < RN; j += 4) {
+            const uint32_t v = (uint32_t)(a4 ^ (j / 4) ^ (line & 7));
+            const float4 t = *reinterpret_cast<const float4 *>(zb + (Kb ^ (v << 4)));
+            f[j] = t.x; f[j + 1] = t.y; f[j + 2] = t.z; f[j + 3] = t.w;
+          }
+        }, acc);
+        __syncwarp();
+        put(gx);  // OUT[q2][q1] over Z[s = q2][q1]
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cdone[st]);
+    }
+  } else {
+    // ---------------- store warps: transpose the finished tile into a [u][g] staging tile (the
+    // StoreFusedShMem layout) and send it with one TMA tensor store to Y[row][u*(W/C) + g0 + g];
+    // 128-byte rows (R = 32) use the 128B swizzle, which the staging writes follow
+    {
+      // ---------------- store warps (direct): chunk-fastest stream-out from registers,
+      // Y[row][u*(W/C) + cb*R + g]: 8 consecutive chunks = 32-byte runs
+      const int sw = warp - NCW;
+      T *Y = reinterpret_cast<T *>(a.Y);
+      const int gl = lane & 7, uq = lane >> 3;
+      for (int it = 0;; ++it) {
+        const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+        if (tile >= a.ntiles) break;
+        const int st = it % a.stages;
+        const uint32_t par = (uint32_t)((it / a.stages) & 1);
+        mbar_wait_sleep(&cdone[st], par);
+        const unsigned char *buf = base + (size_t)st * a.stage_bytes;
+        const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
+        if (a.R % 32 == 0 && rb < a.M && (int64_t)(cbk + 1) * a.R <= a.WC) {
+          // runs of >= 128 bytes: lane = chunk, so every store instruction writes one full 128-byte
+          // line of a u row, and the R/32 lines of a row go out back to back
+          T *yr = Y + (int64_t)rb * a.Wout + (int64_t)cbk * a.R + lane;
+          const int64_t wc = a.WC;
+          const uint32_t gxl = pipe_gx<8, 4>((uint32_t)lane);  // gx depends on g mod 8 only
+#pragma unroll 1
+          for (int u4 = sw; u4 < C / 4; u4 += NSW) {
+            const uint32_t u = (uint32_t)(u4 * 4);
+            T *p = yr + (int64_t)u * wc;
+            for (int h = 0; h < a.R / 32; ++h) {
+              const float4 v = *reinterpret_cast<const float4 *>(buf + (uint32_t)(h * 32 + lane) * CE +
+                                                                 (swz128(u * ES) ^ gxl));
+              p[h * 32] = v.x;
+              p[h * 32 + wc] = v.y;
+              p[h * 32 + 2 * wc] = v.z;
+              p[h * 32 + 3 * wc] = v.w;
+            }
+          }
+        } else
+        for (int oct = 0; oct < a.R / 8; ++oct) {
+          const uint32_t gg = (uint32_t)(oct * 8 + gl);
+          const uint32_t gx = pipe_gx<8, 4>(gg);
+          const unsigned char *ch = buf + gg * CE;
+          const int64_t gcol = (int64_t)cbk * a.R + gg;
+          if (rb < a.M && gcol < a.WC) {
+            T *yg = Y + (int64_t)rb * a.Wout + gcol;
+            const int64_t wc = a.WC;
+#pragma unroll 2
+            for (int u16 = sw; u16 < C / 16; u16 += NSW) {
+              const uint32_t u = (uint32_t)(u16 * 16 + uq * 4);
+              const float4 v = *reinterpret_cast<const float4 *>(ch + (swz128(u * ES) ^ gx));
+              T *p = yg + (int64_t)u * wc;
+              p[0] = v.x;
+              p[wc] = v.y;
+              p[2 * wc] = v.z;
+              p[3 * wc] = v.w;
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+        if (sw == 0) {
+          if (lane == 0) {
+            mbar_wait_sleep(&empty[st], par);
+            fence_proxy_async_smem();
+            issue_load(it + a.stages);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ fp64 two-factor chunks on DMMA (v5)
 //
 // The v4 sandwich OUT = F2^T . (X . F1) per 32 x 32 chunk, fp64, on the FP64 tensor cores (mma.sync
@@ -1324,6 +1564,9 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 8, 64, 8, 4, 2},
     // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 128 * RS * P = 4 chunks): id 30
     {KRON_F64, 32, 128, 1, 5, 0},
+    // v6: fp32 two-factor chunks, warp-specialised (tile = 8192 elements): ids 31..32
+    // (P = 16: 64-chunk tiles = 256-byte output runs; P = 32: 8-chunk tiles = 32-byte runs)
+    {KRON_F32, 16, 512, 2, 6, 0}, {KRON_F32, 32, 256, 1, 6, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1356,6 +1599,8 @@ KernelPFn instance_pipe(int i) {
 
 KernelFn instance_kernel(int i) {
   switch (i) {
+    case 31: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4>;
+    case 32: return kron_fused_gemm2ws_kernel<32, 12, 4, 8, 4>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
     case 7: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
@@ -1519,7 +1764,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   int threads = inst.NT;
   if (inst.warp == 5) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
-    threads = 32 * (8 + 4);  // kron_fused_dmma2_kernel<8, 4>
+    threads = 32 * (8 + 4);
+  } else if (inst.warp == 6) {
+    smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
+    threads = 32 * (12 + 4);
   } else if (inst.warp == 3) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
   } else if (inst.warp == 2 || inst.warp == 4) {
