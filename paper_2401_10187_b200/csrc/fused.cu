@@ -1127,7 +1127,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
 // Y[row][u*(W/C) + g0 + g]) while the compute warps work on the next tiles of the TMA ring (mbarriers:
 // full = landed, cdone = computed, empty = streamed out -> refill).  Output runs are R*4 bytes; the
 // measured write rate of such runs (tools/microbench_scatter.cu: 2.9 TB/s at 32 B, 4.5 TB/s at 128 B,
-// profiles/r02_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
+// profiles/r01_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
 template <int P, int NCW, int RM, int RN, int VA>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                               const __grid_constant__ CUtensorMap tm_out,
