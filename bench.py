@@ -471,8 +471,7 @@ def main():
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
                 "frac": round(ach / alu_peak, 4),
                 "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")}
-    kname = {"fused": "kron_fused_kernel", "generic": "sliced_generic_kernel",
-             "gemm": "kron_dmma_kernel" if es == 8 else "kron_gemm_kernel"}[kind]
+    kname = kron.plan_kernels(M, P, Q, tdt)[dom]
     roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
                  "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
                  "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
@@ -537,7 +536,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
             "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
             "config": {"workload": args.config, "M_per_gpu": M, "P": P, "Q": Q, "K": K, "L": L,
-                       "plan": [list(p) for p in plan], "autotune": tuned,
+                       "plan": [list(p) for p in plan], "kernels": kron.plan_kernels(M, P, Q, tdt), "autotune": tuned,
                        "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,

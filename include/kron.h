@@ -110,6 +110,11 @@ kron_status_t kron_autotune_candidates(int64_t M, int32_t N, const int32_t *P, c
 /* Drop every cached (static or autotuned) plan. */
 kron_status_t kron_plan_cache_clear(void);
 
+/* Kernel (family) that runs pass `pass` of the plan kron_matmul uses, as a NUL-terminated name in
+ * name[0..len) (e.g. "kron_fused_pipe_kernel", "kron_dmma_kernel").  Host only. */
+kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                               int32_t pass, char *name, int32_t len);
+
 /* Algorithmic HBM bytes and FLOPs of the plan:
  *   bytes = sum_passes s*M*(W_in + W_out) + sum_f s*P_f*Q_f,   flops = sum_f 2*M*W_f*Q_f.      */
 kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,

@@ -591,6 +591,28 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
   return KRON_OK;
 }
 
+kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                               int32_t pass, char *name, int32_t len) {
+  if (!name || len < 1) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> pl;
+  kron_status_t st = cached_plan(M, N, P, Q, (int)dtype, &pl);
+  if (st != KRON_OK) return st;
+  if (pass < 0 || pass >= (int32_t)pl->passes.size()) return KRON_ERR_INVALID_ARG;
+  const PassPlan &pp = pl->passes[pass];
+  const char *k = "sliced_generic_kernel";
+  if (pp.kind == KIND_GEMM) {
+    k = pp.variant == 1 ? "kron_dmma_kernel" : "kron_gemm_kernel";
+  } else if (pp.kind == KIND_FUSED) {
+    static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
+                                  "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
+                                  "kron_fused_gemm2ws_kernel"};
+    const int w = fused_instance(pp.variant).warp;
+    k = (w >= 0 && w < 7) ? names[w] : "kron_fused_kernel";
+  }
+  snprintf(name, (size_t)len, "%s", k);
+  return KRON_OK;
+}
+
 kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
                              double *hbm_bytes, double *flops) {
   std::shared_ptr<const Plan> pl;

@@ -55,6 +55,9 @@ _lib.kron_autotune.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, cty
                                ctypes.c_int, ctypes.c_int32, ctypes.c_void_p, _i32p, ctypes.POINTER(ctypes.c_float)]
 _lib.kron_autotune_candidates.restype = ctypes.c_int
 _lib.kron_autotune_candidates.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, _i32p]
+_lib.kron_plan_kernel.restype = ctypes.c_int
+_lib.kron_plan_kernel.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, ctypes.c_int32,
+                                  ctypes.c_char_p, ctypes.c_int32]
 _lib.kron_plan_cache_clear.restype = ctypes.c_int
 _lib.kron_plan_cache_clear.argtypes = []
 
@@ -113,6 +116,17 @@ def plan_describe(M: int, P, Q, dtype):
     _check(_lib.kron_plan_describe(M, len(P), Pa, Qa, dtype_code(dtype), cap, ctypes.byref(n), first, nf, kind),
            "kron_plan_describe")
     return [(first[i], nf[i], KIND_NAMES[kind[i]]) for i in range(n.value)]
+
+
+def plan_kernels(M: int, P, Q, dtype):
+    """Kernel (family) name of every pass of the plan kron_matmul uses."""
+    Pa, Qa = _shape_arrays(P, Q)
+    out = []
+    for i in range(len(plan_describe(M, P, Q, dtype))):
+        buf = ctypes.create_string_buffer(64)
+        _check(_lib.kron_plan_kernel(M, len(P), Pa, Qa, dtype_code(dtype), i, buf, 64), "kron_plan_kernel")
+        out.append(buf.value.decode())
+    return out
 
 
 def plan_cost(M: int, P, Q, dtype):

@@ -164,3 +164,15 @@ def test_autotune_candidates(kron):
     Pa = (ctypes.c_int32 * 2)(2, 2)
     assert lib.kron_autotune(4, 2, Pa, Pa, None, None, None, 0, 3, None, None, None) == 1  # null buffers
     assert lib.kron_plan_cache_clear() == 0
+
+
+def test_plan_kernels(kron):
+    # the kernel family of every pass (bench.py's roofline label, ncu_traffic keys)
+    assert kron.plan_kernels(1024, [8] * 6, [8] * 6, "float32") == ["kron_fused_pipe_kernel"] * 2
+    assert kron.plan_kernels(1024, [32] * 4, [32] * 4, "float64") == ["kron_fused_dmma2_kernel"] * 2
+    assert kron.plan_kernels(320, [128] * 3, [128] * 3, "float64") == ["kron_dmma_kernel"] * 3
+    assert kron.plan_kernels(16, [4, 4], [4, 4], "float32") == ["sliced_generic_kernel"] * 2
+    lib = kron.raw_lib()
+    Pa = (ctypes.c_int32 * 2)(4, 4)
+    buf = ctypes.create_string_buffer(8)
+    assert lib.kron_plan_kernel(16, 2, Pa, Pa, 0, 5, buf, 8) == 1   # no such pass

@@ -15,18 +15,18 @@ done
 timeout 300 python bench.py --impl reference --steps 20 --warmup 3 > $OUT/bench_ref_B.json 2>&1
 for c in B C32 C64 D1 D2 E; do
   timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$c.csv \
-     python bench.py --config $c --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+     python bench.py --config $c --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 done
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 6 -c 1 -o $OUT/prof_B \
-   python bench.py --config B --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config B --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 4 -c 1 -o $OUT/prof_C32 \
-   python bench.py --config C32 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config C32 --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 4 -c 1 -o $OUT/prof_C64 \
-   python bench.py --config C64 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config C64 --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_ -s 6 -c 1 -o $OUT/prof_D1 \
-   python bench.py --config D1 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config D1 --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_ -s 6 -c 1 -o $OUT/prof_D2 \
-   python bench.py --config D2 --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config D2 --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:kron_fused -s 6 -c 2 -o $OUT/prof_E \
-   python bench.py --config E --steps 3 --warmup 3 --no-cpu --no-e2e > /dev/null 2>&1
+   python bench.py --config E --steps 3 --warmup 3 --no-cpu --no-e2e --no-autotune > /dev/null 2>&1
 ls $OUT

@@ -9,6 +9,7 @@ import csv
 import io
 import json
 import os
+import re
 import subprocess
 import sys
 
@@ -74,12 +75,9 @@ def main():
     tpath = os.path.join(os.path.dirname(dst), "ncu_traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
     for d in s:
-        name = d["kernel"]
-        key = ("kron_fused_kernel" if "kron_fused" in name else "kron_gemm_kernel" if "kron_gemm" in name
-               else "kron_dmma_kernel" if "kron_dmma" in name
-               else "sliced_generic_kernel" if "sliced_generic" in name else None)
-        if key and "dram_bytes" in d:
-            traffic.setdefault(cfg, {})[key] = int(d["dram_bytes"])
+        m = re.search(r"(kron_[a-z0-9_]+_kernel|sliced_generic_[a-z_]*kernel)", d["kernel"])
+        if m and "dram_bytes" in d:
+            traffic.setdefault(cfg, {})[m.group(1)] = int(d["dram_bytes"])
     with open(tpath, "w") as f:
         json.dump(traffic, f, indent=1, sort_keys=True)
     print(json.dumps(s, indent=1))
