@@ -269,6 +269,31 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;
     const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;  // always allowed: any chunk size
+    // fp64 64 x 32 factor pairs (GP-style, config D2): one fused DMMA pass per pair (v7)
+    if (dtype == KRON_F64 && p == 64 && q == 32 && f >= 2 && P[f - 2] == 64 && Q[f - 2] == 32 && dmma_ok &&
+        allowed(7) && policy.kcap >= 2 && W % 4096 == 0) {
+      const int iv = fused_find(dtype, 64, 7);
+      if (iv >= 0) {
+        PassPlan pp;
+        pp.kind = KIND_FUSED;
+        pp.variant = iv;
+        pp.first = f;
+        pp.nf = 2;
+        pp.P = 64;
+        pp.Q = 32;
+        pp.C = 4096;
+        pp.Qc = 1024;
+        pp.R = 1;
+        pp.tileM = 1;
+        pp.tileK = 4096;
+        pp.stages = 6;
+        pp.W_in = W;
+        pp.W_out = W / 4096 * 1024;
+        plan->passes.push_back(pp);
+        f -= 2;
+        continue;
+      }
+    }
     if (inst_c >= 0) {
       int run = 1;  // consecutive factors of the same square shape
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
@@ -470,9 +495,9 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x7Fu;
-  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 5) | (1u << 6)),
-                            all & ~((1u << 3) | (1u << 5) | (1u << 6)), (1u << 0) | (1u << 1)};
+  const unsigned all = 0xFFu;
+  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
+                            all & ~((1u << 3) | (1u << 5) | (1u << 6) | (1u << 7)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
   std::vector<Plan> cands;
   auto same = [](const Plan &a, const Plan &b) {
@@ -605,9 +630,9 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
   } else if (pp.kind == KIND_FUSED) {
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
-                                  "kron_fused_gemm2ws_kernel"};
+                                  "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel"};
     const int w = fused_instance(pp.variant).warp;
-    k = (w >= 0 && w < 7) ? names[w] : "kron_fused_kernel";
+    k = (w >= 0 && w < 8) ? names[w] : "kron_fused_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

@@ -1539,6 +1539,174 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
   }
 }
 
+// ------------------------------------------------------------------ fp64 non-square chunk pairs on DMMA (v7)
+//
+// Two consecutive 64 x 32 factors (the GP-style shape of config D2) fused in one pass: a chunk is a
+// 64 x 64 matrix X[s][p] (C = 4096) and the pair is OUT[q2][q1] = sum_s F2[s][q2] * (X . F1)[s][q1]
+// (32 x 32 = Qc = 1024 outputs, u = q2*32 + q1, P:519-523 with P != Q, reading G8).  A chunk is loaded
+// as two TMA boxes of its p-halves, each a [64][32] matrix with 256-byte rows (the v5 layout, so the
+// fragment gathers are conflict free).  Two warps share a chunk: warp h computes Z rows 32h..32h+31
+// (GEMM1, 128 DMMA) and writes them over the p < 32 rows it consumed, then — after a pair barrier —
+// OUT rows 16h..16h+15 (GEMM2, 64 DMMA) into the p >= 32 half.  Four store warps send each finished
+// chunk to Y[row][u*(W/C) + g]; a CTA walks a contiguous range of chunks so consecutive chunks' stores
+// land next to each other while their L2 lines are still resident.
+__device__ __forceinline__ uint32_t rowswz64(uint32_t r, uint32_t c) {  // [rows][64 doubles], thread-filled
+  return r * 512u + ((c * 8u) ^ ((r & 7u) << 4));
+}
+
+template <int NCW, int NSW>
+__global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                              const FusedArgs a) {
+  constexpr int P = 64, Q = 32, C = P * P, CO = Q * Q;
+  constexpr uint32_t CB = C * 8, HB = CB / 2;  // chunk bytes, p-half bytes
+  static_assert(NCW % 2 == 0, "compute warps come in pairs");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char *F1s = base + (size_t)a.stages * CB;  // [p][q1], rowswz32 (64 rows)
+  unsigned char *F2Ts = F1s + P * Q * 8;              // [q2][s] = F2[s][q2], rowswz64 (32 rows)
+  uint64_t *full = reinterpret_cast<uint64_t *>(F2Ts + P * Q * 8);
+  uint64_t *cdone = full + a.stages, *empty = cdone + a.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gq = lane >> 2, tq = lane & 3;
+  {
+    const double *F1 = reinterpret_cast<const double *>(a.F[0]);
+    const double *F2 = reinterpret_cast<const double *>(a.F[1]);
+    for (int i = tid; i < P * Q; i += (NCW + NSW) * 32) {
+      const uint32_t r = (uint32_t)i / Q, c = (uint32_t)i % Q;
+      *reinterpret_cast<double *>(F1s + rowswz32(r, c)) = F1[i];   // F1[p = r][q1 = c]
+      *reinterpret_cast<double *>(F2Ts + rowswz64(c, r)) = F2[i];  // F2[s = r][q2 = c] -> F2T[c][r]
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], 2);
+      mbar_init(&empty[s], NSW);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  // a CTA walks the contiguous chunk range [t0, t1)
+  const int64_t per = (a.ntiles + gridDim.x - 1) / gridDim.x;
+  const int64_t t0 = (int64_t)blockIdx.x * per;
+  const int64_t t1 = t0 + per < a.ntiles ? t0 + per : a.ntiles;
+  auto issue_load = [&](int it) {
+    const int64_t tile = t0 + it;
+    if (tile >= t1) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), g = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * CB;
+    mbar_arrive_expect_tx(&full[st], CB);
+    tma_load_5d(dst, &tm_in, &full[st], 0, 0, 0, g, rb);
+    tma_load_5d(dst + HB, &tm_in, &full[st], 0, 2, 0, g, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    const int pair = warp >> 1, h = warp & 1;
+    for (int it = pair; t0 + it < t1; it += NCW / 2) {
+      const int st = it % a.stages;
+      mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
+      unsigned char *cb0 = base + (size_t)st * CB;
+      double acc[2][4][4];
+      // ---- GEMM1 (rows 32h..32h+31): Z[s][q1] = sum_p X[s][p] F1[p][q1]; p-half hp at cb0 + hp*HB
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+#pragma unroll
+      for (int hp = 0; hp < 2; ++hp) {
+        const unsigned char *xb = cb0 + hp * HB;
+#pragma unroll
+        for (int k0 = 0; k0 < 32; k0 += 4) {
+          double a0[2], a1[2], b[4];
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const uint32_t r = (uint32_t)(h * 32 + mt * 16 + gq);
+            a0[mt] = *reinterpret_cast<const double *>(xb + rowswz32(r, k0 + tq));
+            a1[mt] = *reinterpret_cast<const double *>(xb + rowswz32(r + 8, k0 + tq));
+          }
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+            b[nt] = *reinterpret_cast<const double *>(F1s + rowswz32(hp * 32 + k0 + tq, nt * 8 + gq));
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[mt][nt], a0[mt], a1[mt], b[nt]);
+        }
+      }
+      __syncwarp();
+      // Z rows of this warp over the p < 32 half of the rows it consumed (same [64][32] layout)
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int v1 = 0; v1 < 2; ++v1)
+            *reinterpret_cast<double2 *>(cb0 + rowswz32(h * 32 + mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+                make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
+      named_bar_sync(2 + pair, 64);  // both halves of Z written (and both GEMM1s done with the p >= 32 half)
+      // ---- GEMM2 (rows q2 = 16h..16h+15): OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
+      double acc2[4][4];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc2[nt][e] = 0.0;
+#pragma unroll
+      for (int k0 = 0; k0 < 64; k0 += 4) {
+        const uint32_t r = (uint32_t)(h * 16 + gq);
+        const double a0 = *reinterpret_cast<const double *>(F2Ts + rowswz64(r, k0 + tq));
+        const double a1 = *reinterpret_cast<const double *>(F2Ts + rowswz64(r + 8, k0 + tq));
+        double b[4];
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswz32(k0 + tq, nt * 8 + gq));
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc2[nt], a0, a1, b[nt]);
+      }
+      // OUT rows into the p >= 32 half (no longer read by anyone); [32][32], rowswz32
+      unsigned char *ob = cb0 + HB;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int v1 = 0; v1 < 2; ++v1)
+          *reinterpret_cast<double2 *>(ob + rowswz32(h * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+              make_double2(acc2[nt][2 * v1], acc2[nt][2 * v1 + 1]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&cdone[st]);
+    }
+  } else {
+    // ---------------- store warps: OUT[u] -> Y[row][u*(W/C) + g]
+    const int sw = warp - NCW;
+    double *Y = reinterpret_cast<double *>(a.Y);
+    for (int it = 0; t0 + it < t1; ++it) {
+      const int64_t tile = t0 + it;
+      const int st = it % a.stages;
+      const uint32_t par = (uint32_t)((it / a.stages) & 1);
+      mbar_wait_sleep(&cdone[st], par);
+      const unsigned char *ob = base + (size_t)st * CB + HB;
+      const int rb = (int)(tile / a.tiles_k), g = (int)(tile - (int64_t)rb * a.tiles_k);
+      double *yg = Y + (int64_t)rb * a.Wout + g;
+#pragma unroll 4
+      for (int u = sw * 32 + lane; u < CO; u += NSW * 32)
+        yg[(int64_t)u * a.WC] = *reinterpret_cast<const double *>(ob + rowswz32((uint32_t)u / Q, (uint32_t)u % Q));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (sw == 0) {
+        if (lane == 0) {
+          mbar_wait_sleep(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + a.stages);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
@@ -1567,6 +1735,8 @@ const FusedInstance kInstances[] = {
     // v6: fp32 two-factor chunks, warp-specialised (tile = 8192 elements): ids 31..32
     // (P = 16: 64-chunk tiles = 256-byte output runs; P = 32: 8-chunk tiles = 32-byte runs)
     {KRON_F32, 16, 512, 2, 6, 0}, {KRON_F32, 32, 256, 1, 6, 0},
+    // v7: fp64 64 x 32 factor pairs on DMMA (one chunk of 4096 per tile): id 33
+    {KRON_F64, 64, 64, 1, 7, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1577,6 +1747,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
     case 30: return kron_fused_dmma2_kernel<8, 4>;
+    case 33: return kron_fused_dmma2g_kernel<8, 4>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -1720,6 +1891,26 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.stage_bytes = (a.tile_bytes + 1023u) & ~1023u;
   a.stages = pp.stages;
 
+  if (inst.warp == 7) {
+    // 5-D map over X[m][g][s][p/16][p%16]; box = one p-half of one chunk ([64][2][16] = 16 KB)
+    CUtensorMap t5;
+    uint64_t dims[5] = {16, 4, 64, (uint64_t)WC, (uint64_t)M};
+    uint64_t strides[4] = {128, 512, 32768, (uint64_t)W * 8};
+    uint32_t box[5] = {16, 2, 64, 1, 1};
+    if (!encode_tmap(&t5, dtype, 5, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
+    a.Y = out;
+    a.WC = WC;
+    a.Wout = Wout;
+    a.M = M;
+    const size_t smem7 = 1024 + (size_t)a.stages * 32768 + 2 * 64 * 32 * 8 + 24 * (size_t)a.stages;
+    Kernel4Fn k7 = instance_kernel4(pp.variant);
+    const int slots = kernel_slots((const void *)k7, 32 * (8 + 4), smem7);
+    if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+    int64_t grid = slots;
+    if (grid > a.ntiles) grid = a.ntiles;
+    k7<<<(unsigned)grid, 32 * (8 + 4), smem7, (cudaStream_t)stream>>>(t5, a);
+    return (int)cudaGetLastError();
+  }
   CUtensorMap tin, tout;
   {
     uint64_t dims[3] = {(uint64_t)line, (uint64_t)(W / line), (uint64_t)M};

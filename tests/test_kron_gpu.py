@@ -59,7 +59,9 @@ SMALL = [
     (7, [3, 5, 2], [2, 4, 3]),            # odd non-square -> generic
     (4, [8, 2], [2, 8]),                  # mixed widths (G2)
     (6, [5, 8, 8, 8], [5, 8, 8, 8]),      # odd leading factor + fused 8-run
-    (3, [64, 64], [32, 32]),              # non-square large P
+    (3, [64, 64], [32, 32]),              # non-square large P (fp64: fused 64x32 pair on DMMA)
+    (4, [64] * 3, [32] * 3),              # config D2 shape, small M (fused pair + single factor)
+    (3, [2, 64, 64], [2, 32, 32]),        # fused 64x32 pair behind a tiny leading factor
     (2, [128, 16], [128, 16]),            # large P then small
     (4, [7], [9]),                        # N = 1: plain GEMM
     (3, [1, 4, 1], [2, 4, 1]),            # P_i or Q_i = 1
