@@ -209,11 +209,13 @@ int gemm_pick(int dtype, int Q) {
 // (3-D boxes {16, 2, rows} with the 128B swizzle: the two 128-byte lines of a row get different XOR
 // patterns, which makes both fragment gathers bank-conflict free); the epilogue writes C fragments
 // straight to Y[m, q*S + s] (8 consecutive slices = 64 bytes per column).
-template <int NWARP, int NS>
+template <int NWARP, int NS, int WN>
 __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __grid_constant__ CUtensorMap tm_a,
                                                                        const __grid_constant__ CUtensorMap tm_b,
                                                                        double *__restrict__ Y, const GemmArgs g) {
-  constexpr int BK = 32, BN = 32, WTM = 32, BM = NWARP * WTM;
+  // WN warps along q (BN = 32*WN columns per CTA tile): with WN = 4 a Q = 128 factor is one column tile,
+  // so every A row block is fetched from HBM once instead of once per 32 columns
+  constexpr int BK = 32, WTM = 32, BM = (NWARP / WN) * WTM, BN = WN * 32;
   constexpr uint32_t A_BYTES = BM * BK * 8, B_BYTES = BK * BN * 8, STAGE = A_BYTES + B_BYTES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -254,13 +256,15 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
         unsigned char *sa = base + st * STAGE;
         mbar_arrive_expect_tx(&full[st], STAGE);
         tma_load_3d(sa, &tm_a, &full[st], 0, k * (BK / 16), (int)(mt * BM));
-        tma_load_3d(sa + A_BYTES, &tm_b, &full[st], 0, nt * (BN / 16), k * BK);
+        for (int j = 0; j < WN; ++j)  // one [BK][32] slab (256-byte rows) per warp column
+          tma_load_3d(sa + A_BYTES + j * (BK * 256), &tm_b, &full[st], 0, nt * (BN / 16) + 2 * j, k * BK);
       }
     }
     return;
   }
 
-  // A fragment bases: rows r = warp*32 + mt*16 + gq + 8v, two 128-byte lines (k < 16, k >= 16)
+  const int wm = warp / WN, wn = warp % WN;
+  // A fragment bases: rows r = wm*32 + mt*16 + gq + 8v, two 128-byte lines (k < 16, k >= 16)
   uint32_t abase[2][2][2];
 #pragma unroll
   for (int mt = 0; mt < 2; ++mt)
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
     for (int v = 0; v < 2; ++v)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const uint32_t row = (uint32_t)(warp * WTM + mt * 16 + gq + 8 * v);
+        const uint32_t row = (uint32_t)(wm * WTM + mt * 16 + gq + 8 * v);
         const uint32_t line = 2 * row + h;
         abase[mt][v][h] = line * 128u + (((uint32_t)tq * 8u) ^ ((line & 7u) << 4));
       }
@@ -297,7 +301,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
     const int st = (int)(z % NS);
     mbar_wait(&full[st], (uint32_t)((z / NS) & 1));
     const unsigned char *sa = base + st * STAGE;
-    const unsigned char *sb = sa + A_BYTES;
+    const unsigned char *sb = sa + A_BYTES + wn * (BK * 256);
 #pragma unroll
     for (int k0 = 0; k0 < BK; k0 += 4) {
       const int h = k0 >> 4;
@@ -323,7 +327,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
       for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
         for (int v1 = 0; v1 < 2; ++v1) {
-          const int64_t r = mt0 * BM + warp * WTM + mt * 16 + gq + 8 * v1;
+          const int64_t r = mt0 * BM + wm * WTM + mt * 16 + gq + 8 * v1;
           if (r < g.rows) {
             const int64_t m = r / g.S, s = r - m * g.S;
             double *yrow = Y + m * g.Wout + s;
@@ -331,7 +335,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
             for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
               for (int v0 = 0; v0 < 2; ++v0) {
-                const int q = ntile * BN + nt * 8 + 2 * tq + v0;
+                const int q = ntile * BN + wn * 32 + nt * 8 + 2 * tq + v0;
                 if (q < g.Q) yrow[(int64_t)q * g.S] = acc[mt][nt][v1 * 2 + v0];
               }
           }
@@ -346,8 +350,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1) kron_dmma_kernel(const __
   }
 }
 
-int launch_dmma(const PassPlan &pp, int64_t M, const void *in, void *out, const void *F, void *stream) {
-  constexpr int NWARP = 8, NS = 3, BK = 32, BN = 32, BM = NWARP * 32;
+template <int NWARP, int NS, int WN>
+int launch_dmma_t(const PassPlan &pp, int64_t M, const void *in, void *out, const void *F, void *stream) {
+  constexpr int BK = 32, BN = WN * 32, BM = (NWARP / WN) * 32;
   GemmArgs g{};
   g.S = pp.W_in / pp.P;
   g.rows = M * g.S;
@@ -372,13 +377,18 @@ int launch_dmma(const PassPlan &pp, int64_t M, const void *in, void *out, const 
     if (!encode_tmap(&tb, KRON_F64, 3, F, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
   }
   const size_t smem = 1024 + NS * ((size_t)BM * BK * 8 + (size_t)BK * BN * 8) + 16 * NS;
-  auto k = kron_dmma_kernel<NWARP, NS>;
+  auto k = kron_dmma_kernel<NWARP, NS, WN>;
   const int slots = kernel_slots((const void *)k, (NWARP + 1) * 32, smem);
   if (slots < 1) return (int)cudaErrorInvalidConfiguration;
   int64_t grid = slots;
   if (grid > g.ntiles) grid = g.ntiles;
   k<<<(unsigned)grid, (NWARP + 1) * 32, smem, (cudaStream_t)stream>>>(ta, tb, (double *)out, g);
   return (int)cudaGetLastError();
+}
+
+int launch_dmma(const PassPlan &pp, int64_t M, const void *in, void *out, const void *F, void *stream) {
+  if (pp.Q % 128 == 0) return launch_dmma_t<8, 4, 4>(pp, M, in, out, F, stream);
+  return launch_dmma_t<8, 3, 1>(pp, M, in, out, F, stream);
 }
 }  // namespace
 

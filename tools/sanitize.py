@@ -14,26 +14,35 @@ import synth  # noqa: E402
 from paper_2401_10187_b200 import kron  # noqa: E402
 
 CASES = [
-    (9, [8] * 6, np.float32),        # v3 factor pipeline (3,3)
-    (3, [32] * 2, np.float32),       # v4 chunk GEMMs (2)
-    (2, [16] * 3, np.float32),       # v4 (2) + v2 (1)
-    (2, [32] * 2, np.float64),       # v4 fp64
-    (5, [4] * 5, np.float64),        # v3 fp64 / v2
-    (3, [16] * 3, np.float64),       # v1/v2 fp64
-    (2, [64, 64], np.float64),       # gemm
-    (3, [3, 5], np.float32),         # generic
+    (9, [8] * 6, [8] * 6, np.float32),          # v3 factor pipeline (3,3)
+    (3, [32] * 2, [32] * 2, np.float32),        # v6 warp-specialised chunk pair, P = 32
+    (2, [16] * 4, [16] * 4, np.float32),        # v6, P = 16 (64-chunk tiles)
+    (2, [16] * 3, [16] * 3, np.float32),        # v4/v6 (2) + v2 (1)
+    (2, [32] * 2, [32] * 2, np.float64),        # v5 DMMA chunk pair
+    (3, [16] * 2, [16] * 2, np.float64),        # v4 fp64
+    (2, [64] * 3, [32] * 3, np.float64),        # v7 64x32 pair on DMMA + DMMA gemm
+    (5, [4] * 5, [4] * 5, np.float64),          # v3 fp64 / v2
+    (3, [16] * 3, [16] * 3, np.float64),        # v1/v2 fp64
+    (2, [64, 64], [64, 64], np.float64),        # DMMA gemm
+    (2, [64, 64], [64, 64], np.float32),        # FFMA2 gemm
+    (3, [3, 5], [4, 2], np.float32),            # generic
 ]
 
 
 def main():
     dev = torch.device("cuda:0")
-    for M, P, dt in CASES:
+    for M, P, Q, dt in CASES:
         seed = synth.SEED_BASE + 77
         X = synth.matrix(M, int(np.prod(P)), seed, 0, "urand", dt)
-        Fs = synth.factors(P, P, seed, "urand", dt)
+        Fs = synth.factors(P, Q, seed, "urand", dt)
         Y = kron.matmul(torch.from_numpy(X).to(dev), [torch.from_numpy(f).to(dev) for f in Fs])
         torch.cuda.synchronize()
-        print("ok", M, P, np.dtype(dt).name, kron.plan_describe(M, P, P, np.dtype(dt).name), float(Y.sum()))
+        print("ok", M, P, Q, np.dtype(dt).name, kron.plan_kernels(M, P, Q, np.dtype(dt).name), float(Y.sum()))
+    # the autotuner runs every candidate plan of one shape
+    X = torch.from_numpy(synth.matrix(3, 32 ** 2, 5, 0, "urand", np.float32)).to(dev)
+    _, n, _ = kron.autotune(X, [torch.from_numpy(f).to(dev) for f in synth.factors([32] * 2, [32] * 2, 5, "urand", np.float32)], reps=1)
+    torch.cuda.synchronize()
+    print("ok autotune", n, "candidates")
     ctx = kron.DistContext("virtual", GM=2, GK=2)
     X = synth.matrix(4, 16 ** 3, 1, 0, "urand", np.float32)
     blocks = [torch.from_numpy(np.ascontiguousarray(X[(r // 2) * 2:(r // 2) * 2 + 2, (r % 2) * 2048:(r % 2) * 2048 + 2048])).to(dev)
