@@ -1161,8 +1161,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&cdone[s], UPT);
-      mbar_init(&empty[s], NSW);
+      mbar_init(&cdone[s], UPT * 32);
+      mbar_init(&empty[s], NSW * 32);
     }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
@@ -1284,7 +1284,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
         put(gx);  // OUT[q2][q1] over Z[s = q2][q1]
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&cdone[st]);
+      mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
     }
   } else {
     // ---------------- store warps: transpose the finished tile into a [u][g] staging tile (the
@@ -1345,7 +1345,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
+        mbar_arrive(&empty[st]);
         if (sw == 0) {
           if (lane == 0) {
             mbar_wait_sleep(&empty[st], par);
@@ -1403,8 +1403,8 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&cdone[s], CPT);
-      mbar_init(&empty[s], NSW);
+      mbar_init(&cdone[s], CPT * 32);
+      mbar_init(&empty[s], NSW * 32);
     }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
@@ -1499,7 +1499,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
             *reinterpret_cast<double2 *>(cb0 + (rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
                 make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&cdone[st]);
+      mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
     }
   } else {
     // ---------------- store warps: chunk-fastest stream-out, Y[row][u*(W/C) + cb*R + g]
@@ -1526,7 +1526,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      mbar_arrive(&empty[st]);
       if (sw == 0) {
         if (lane == 0) {
           mbar_wait(&empty[st], par);
@@ -1580,8 +1580,8 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&cdone[s], 2);
-      mbar_init(&empty[s], NSW);
+      mbar_init(&cdone[s], 2 * 32);
+      mbar_init(&empty[s], NSW * 32);
     }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
@@ -1676,7 +1676,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
           *reinterpret_cast<double2 *>(ob + rowswz32(h * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
               make_double2(acc2[nt][2 * v1], acc2[nt][2 * v1 + 1]);
       __syncwarp();
-      if (lane == 0) mbar_arrive(&cdone[st]);
+      mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
     }
   } else {
     // ---------------- store warps: OUT[u] -> Y[row][u*(W/C) + g]
@@ -1694,7 +1694,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
       for (int u = sw * 32 + lane; u < CO; u += NSW * 32)
         yg[(int64_t)u * a.WC] = *reinterpret_cast<const double *>(ob + rowswz32((uint32_t)u / Q, (uint32_t)u % Q));
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
+      mbar_arrive(&empty[st]);
       if (sw == 0) {
         if (lane == 0) {
           mbar_wait_sleep(&empty[st], par);

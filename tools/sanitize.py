@@ -15,15 +15,16 @@ from paper_2401_10187_b200 import kron  # noqa: E402
 
 CASES = [
     (9, [8] * 6, [8] * 6, np.float32),          # v3 factor pipeline (3,3)
-    (3, [32] * 2, [32] * 2, np.float32),        # v6 warp-specialised chunk pair, P = 32
+    (2, [32] * 3, [32] * 3, np.float32),        # v6 warp-specialised chunk pair, P = 32 (+ v2)
     (2, [16] * 4, [16] * 4, np.float32),        # v6, P = 16 (64-chunk tiles)
     (2, [16] * 3, [16] * 3, np.float32),        # v4/v6 (2) + v2 (1)
-    (2, [32] * 2, [32] * 2, np.float64),        # v5 DMMA chunk pair
+    (2, [32] * 3, [32] * 3, np.float64),        # v5 DMMA chunk pair (+ v2)
     (3, [16] * 2, [16] * 2, np.float64),        # v4 fp64
     (2, [64] * 3, [32] * 3, np.float64),        # v7 64x32 pair on DMMA + DMMA gemm
     (5, [4] * 5, [4] * 5, np.float64),          # v3 fp64 / v2
     (3, [16] * 3, [16] * 3, np.float64),        # v1/v2 fp64
-    (2, [64, 64], [64, 64], np.float64),        # DMMA gemm
+    (2, [64, 64], [64, 64], np.float64),        # DMMA gemm (32-column tiles)
+    (2, [128, 128], [128, 128], np.float64),    # DMMA gemm (128-column tiles)
     (2, [64, 64], [64, 64], np.float32),        # FFMA2 gemm
     (3, [3, 5], [4, 2], np.float32),            # generic
 ]
