@@ -40,8 +40,8 @@ def main():
         torch.cuda.synchronize()
         print("ok", M, P, Q, np.dtype(dt).name, kron.plan_kernels(M, P, Q, np.dtype(dt).name), float(Y.sum()))
     # the autotuner runs every candidate plan of one shape
-    X = torch.from_numpy(synth.matrix(3, 32 ** 2, 5, 0, "urand", np.float32)).to(dev)
-    _, n, _ = kron.autotune(X, [torch.from_numpy(f).to(dev) for f in synth.factors([32] * 2, [32] * 2, 5, "urand", np.float32)], reps=1)
+    X = torch.from_numpy(synth.matrix(2, 16 ** 4, 5, 0, "urand", np.float32)).to(dev)
+    _, n, _ = kron.autotune(X, [torch.from_numpy(f).to(dev) for f in synth.factors([16] * 4, [16] * 4, 5, "urand", np.float32)], reps=1)
     torch.cuda.synchronize()
     print("ok autotune", n, "candidates")
     ctx = kron.DistContext("virtual", GM=2, GK=2)
