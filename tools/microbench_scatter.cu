@@ -23,6 +23,29 @@ __global__ void scatter(const float *__restrict__ X, float *__restrict__ Y, long
   }
 }
 
+// same pattern with 16-byte stores: lane = 4 consecutive chunks of one u
+__global__ void scatter4(const float *__restrict__ X, float *__restrict__ Y, long M, long W, int C, int R) {
+  extern __shared__ float tile[];
+  const long WC = W / C, tpr = W / ((long)R * C), tiles = M * tpr;
+  for (long t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const long row = t / tpr, cb = t - row * tpr;
+    const float4 *src = reinterpret_cast<const float4 *>(X + row * W + cb * (long)R * C);
+    __syncthreads();
+    for (int i = threadIdx.x; i < R * C / 4; i += blockDim.x) reinterpret_cast<float4 *>(tile)[i] = src[i];
+    __syncthreads();
+    float *dst = Y + row * W + cb * R;
+    for (int i = threadIdx.x; i < R * C / 4; i += blockDim.x) {
+      const int g4 = i % (R / 4), u = i / (R / 4);
+      float4 v;
+      v.x = tile[(4 * g4) * C + u];
+      v.y = tile[(4 * g4 + 1) * C + u];
+      v.z = tile[(4 * g4 + 2) * C + u];
+      v.w = tile[(4 * g4 + 3) * C + u];
+      *reinterpret_cast<float4 *>(dst + (long)u * WC + 4 * g4) = v;
+    }
+  }
+}
+
 __global__ void copy(const float4 *__restrict__ X, float4 *__restrict__ Y, long n4) {
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n4; i += (long)gridDim.x * blockDim.x) Y[i] = X[i];
 }
@@ -59,6 +82,16 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
     }
     printf("{\"kind\": \"scatter\", \"C\": %d, \"R\": %d, \"run_bytes\": %d, \"stride_bytes\": %ld, \"GBps\": %.1f}\n",
+           c.C, c.R, c.R * 4, W / c.C * 4, 2.0 * n * 4 / ms / 1e6);
+    cudaFuncSetAttribute(scatter4, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaEventRecord(a);
+      scatter4<<<148 * per_sm, 512, smem>>>(X, Y, M, W, c.C, c.R);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      cudaEventElapsedTime(&ms, a, b);
+    }
+    printf("{\"kind\": \"scatter_st128\", \"C\": %d, \"R\": %d, \"run_bytes\": %d, \"stride_bytes\": %ld, \"GBps\": %.1f}\n",
            c.C, c.R, c.R * 4, W / c.C * 4, 2.0 * n * 4 / ms / 1e6);
   }
   printf("{\"status\": \"%s\"}\n", cudaGetErrorString(cudaGetLastError()));
