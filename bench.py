@@ -50,6 +50,7 @@ CONFIGS = {
 # 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz; FP64 = half the FP32 lanes.
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
 FP64_PEAK_TFLOPS = FP32_PEAK_TFLOPS / 2
+MMA_TF32_TFLOPS = 274.6  # legacy mma.sync m16n8k8 TF32, measured (profiles/r01_microbench_mma.jsonl)
 HBM_FALLBACK_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only without MEASURED_PEAKS.json
 
 REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -358,6 +359,8 @@ def main():
                     help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
                          "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
     ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
+    ap.add_argument("--mode", default=None, choices=["3xtf32"],
+                    help="fp32 configs only: the separately reported 3xTF32 tensor-core mode (NEXT-4)")
     ap.add_argument("--autotune", action=argparse.BooleanOptionalAction, default=True,
                     help="autotune the pass plan before warm-up (P:599-619); --no-autotune = static plan")
     ap.add_argument("--sweep", default=None, choices=["table3", "table4"],
@@ -393,6 +396,9 @@ def main():
 
     cfg, M, P, Q, dtn = CONFIGS[args.config]
     dt = np.float32 if dtn == "float32" else np.float64
+    mode = args.mode
+    if mode and dt != np.float32:
+        ap.error("--mode 3xtf32 applies to the fp32 configs (B, C32, E)")
     tdt = torch.float32 if dt == np.float32 else torch.float64
     es = 4 if dt == np.float32 else 8
     seed = synth.SEED_BASE + cfg
@@ -408,11 +414,11 @@ def main():
     tuned = None
     if args.autotune:
         # time the candidate plans on these buffers, keep the fastest (untimed, before warm-up)
-        _, ncand, best = kron.autotune(X, Fs, Y, reps=3)
+        _, ncand, best = kron.autotune(X, Fs, Y, reps=3, mode=mode)
         tuned = {"candidates": ncand, "best_ms": round(best, 5)}
-    wsz = kron.workspace_size(M, P, Q, tdt)
+    wsz = kron.workspace_size(M, P, Q, tdt, mode)
     work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
-    plan = kron.plan_describe(M, P, Q, tdt)
+    plan = kron.plan_describe(M, P, Q, tdt, mode)
     npass = len(plan)
     W = widths(P, Q)
 
@@ -423,7 +429,7 @@ def main():
         return evs
 
     for _ in range(args.warmup):
-        kron.matmul_ws(X, Fs, Y, work)
+        kron.matmul_ws(X, Fs, Y, work, mode=mode)
     torch.cuda.synchronize()
 
     pass_events = [mk_events(npass + 1) for _ in range(args.steps)]
@@ -434,7 +440,7 @@ def main():
     with ClockSampler(local) as clocks:
         t_start.record(stream)
         for k in range(args.steps):
-            kron.matmul_ws_events(X, Fs, Y, work, [e.cuda_event for e in pass_events[k]])
+            kron.matmul_ws_events(X, Fs, Y, work, [e.cuda_event for e in pass_events[k]], mode=mode)
         t_end.record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -460,6 +466,10 @@ def main():
     alg_flops = sum(2.0 * M * W[f] * Q[f - 1] for f in range(first, first - nf, -1))
     hbm_peak, hbm_src = measured_peaks()
     alu_peak = FP32_PEAK_TFLOPS if dt == np.float32 else FP64_PEAK_TFLOPS
+    alu_src = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")
+    if mode and kron.plan_kernels(M, P, Q, tdt, mode)[dom] == "kron_fused_tf32x3_kernel":
+        # the 3xTF32 pass runs on the warp MMA: measured mma.sync TF32 rate / 3 MMAs per product
+        alu_peak, alu_src = MMA_TF32_TFLOPS / 3, "measured mma.sync TF32 (profiles/r01_microbench_mma.jsonl) / 3"
     t_dom = pass_ms[dom] / 1e3
     t_hbm, t_alu = alg_bytes / (hbm_peak * 1e9), alg_flops / (alu_peak * 1e12)
     if t_hbm >= t_alu:
@@ -470,15 +480,15 @@ def main():
         ach = alg_flops / t_dom / 1e12
         roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
                 "frac": round(ach / alu_peak, 4),
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")}
-    kname = kron.plan_kernels(M, P, Q, tdt)[dom]
+                "peak_source": alu_src}
+    kname = kron.plan_kernels(M, P, Q, tdt, mode)[dom]
     roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
                  "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
                  "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
                  "traffic": ncu_traffic(args.config, kname)})
 
     # whole-step roofline (all passes): T_roof = max(B_alg/BW, F_alg/peak)
-    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt)
+    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt, mode)
     t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12))
     step_frac = t_roof / (ms / args.steps / 1e3)
 
@@ -499,7 +509,7 @@ def main():
             Xd.copy_(Xh, non_blocking=True)
             for a, b in zip(Fd, Fh):
                 a.copy_(b, non_blocking=True)
-            kron.matmul(Xd, Fd, out=Yd)
+            kron.matmul(Xd, Fd, out=Yd, mode=mode)
             Yh.copy_(Yd, non_blocking=True)
 
         e2e_step()
@@ -534,9 +544,10 @@ def main():
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+            **({"mode": "3xtf32 (fp32 data, TF32 split tensor-core MMAs; reported separately)"} if mode else {}),
             "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
             "config": {"workload": args.config, "M_per_gpu": M, "P": P, "Q": Q, "K": K, "L": L,
-                       "plan": [list(p) for p in plan], "kernels": kron.plan_kernels(M, P, Q, tdt), "autotune": tuned,
+                       "plan": [list(p) for p in plan], "kernels": kron.plan_kernels(M, P, Q, tdt, mode), "autotune": tuned,
                        "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
                        "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,

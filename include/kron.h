@@ -35,7 +35,11 @@
 extern "C" {
 #endif
 
-typedef enum { KRON_F32 = 0, KRON_F64 = 1 } kron_dtype_t;
+/* KRON_F32_3XTF32: fp32 data (same layout and buffers as KRON_F32) computed in the separately reported
+ * 3xTF32 tensor-core mode: P = 32 factor pairs run on the warp MMA with the
+ * split x = hi + lo per operand (~22-bit products, fp32 accumulation); every other pass uses the fp32
+ * CUDA-core kernels.  Not the default: KRON_F32 is the reference fp32 arithmetic. */
+typedef enum { KRON_F32 = 0, KRON_F64 = 1, KRON_F32_3XTF32 = 2 } kron_dtype_t;
 
 typedef enum {
   KRON_OK = 0,
@@ -153,6 +157,7 @@ kron_status_t kron_dist_nccl_unique_id(void *out128);
 /* Collective over the context's ranks: every rank calls it with identical M, N, P, Q, dtype.
  * NCCL backend: X_local / Y_local are this rank's blocks.
  * Virtual backend: X_local / Y_local are host arrays of GM*GK device pointers, one per rank.
+ * dtype KRON_F32 or KRON_F64 (KRON_F32_3XTF32 -> KRON_ERR_UNSUPPORTED).
  * Errors: GM !| M, GK !| K, GK !| L or no legal round plan -> KRON_ERR_DIST_LAYOUT (shape-only,
  * so every rank returns the same status).  NCCL failures -> KRON_ERR_NCCL.                    */
 kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X_local,

@@ -18,7 +18,7 @@ namespace kron {
 
 namespace {
 
-int es_of(int dtype) { return dtype == KRON_F32 ? 4 : 8; }
+int es_of(int dtype) { return dtype == KRON_F64 ? 8 : 4; }
 
 bool mul_ok(int64_t a, int64_t b, int64_t lim, int64_t *out) {
   if (a != 0 && b > lim / a) return false;
@@ -62,7 +62,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
     if (W * es >= (int64_t(1) << 32)) return false;  // 32-bit in-row store offsets
   }
-  if (inst.warp == 6) {
+  if (inst.warp == 6 || inst.warp == 8) {
     // warp-specialised fp32 chunk pairs: two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
   }
@@ -77,9 +77,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 5 || inst.warp == 6) {
-    // one warp-specialised CTA per SM
-    stages = (int)((220 * 1024 - 2 * (int64_t)p * p * es) / stage);
+  if (inst.warp == 5 || inst.warp == 6 || inst.warp == 8) {
+    // one warp-specialised CTA per SM (v8 keeps hi/lo splits of both factors)
+    stages = (int)((220 * 1024 - (inst.warp == 8 ? 4 : 2) * (int64_t)p * p * es) / stage);
     if (stages > 8) stages = 8;
   } else if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
@@ -218,7 +218,7 @@ kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, vo
 
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   if (M < 0 || N < 1 || N > kMaxFactors || !P || !Q) return KRON_ERR_INVALID_ARG;
-  if (dtype != KRON_F32 && dtype != KRON_F64) return KRON_ERR_INVALID_ARG;
+  if (dtype != KRON_F32 && dtype != KRON_F64 && dtype != KRON_F32_3XTF32) return KRON_ERR_INVALID_ARG;
   for (int i = 0; i < N; ++i)
     if (P[i] < 1 || Q[i] < 1) return KRON_ERR_INVALID_ARG;
   const int64_t lim = (int64_t)1 << 50;  // elements per row; beyond any HBM
@@ -241,6 +241,9 @@ kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan, int64_t lead,
                         const PlanPolicy &policy) {
   kron_status_t st = validate(M, N, P, Q, dtype);
+  // 3xTF32 mode: fp32 data; P = 32 pairs go to the tensor-core kernel, everything else as KRON_F32
+  const bool tf32x3 = dtype == KRON_F32_3XTF32;
+  if (tf32x3) dtype = KRON_F32;
   if (st != KRON_OK) return st;
   if (lead < 1) return KRON_ERR_INVALID_ARG;
   plan->N = N;
@@ -264,6 +267,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const bool dmma_ok = policy.dmma && !getenv("KRON_NO_DMMA");
     auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
+    const int inst_t = (tf32x3 && p == q && allowed(8)) ? fused_find(dtype, p, 8) : -1;
     const int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
@@ -299,6 +303,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_t >= 0 && fused_geometry(fused_instance(inst_t), k, W, Mp, pp)) return inst_t;
         if (inst_d >= 0 && fused_geometry(fused_instance(inst_d), k, W, Mp, pp)) return inst_d;
         if (inst_s >= 0 && fused_geometry(fused_instance(inst_s), k, W, Mp, pp)) return inst_s;
         if (inst_g >= 0 && fused_geometry(fused_instance(inst_g), k, W, Mp, pp)) return inst_g;
@@ -495,7 +500,7 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0xFFu;
+  const unsigned all = 0x1FFu;
   const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
                             all & ~((1u << 3) | (1u << 5) | (1u << 6) | (1u << 7)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
@@ -630,9 +635,9 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
   } else if (pp.kind == KIND_FUSED) {
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
-                                  "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel"};
+                                  "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel", "kron_fused_tf32x3_kernel"};
     const int w = fused_instance(pp.variant).warp;
-    k = (w >= 0 && w < 8) ? names[w] : "kron_fused_kernel";
+    k = (w >= 0 && w < 9) ? names[w] : "kron_fused_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

@@ -340,6 +340,7 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
   if (!ctx) return KRON_ERR_INVALID_ARG;
   kron_status_t st = validate(M, N, P, Q, (int)dtype);
   if (st != KRON_OK) return st;
+  if (dtype == KRON_F32_3XTF32) return KRON_ERR_UNSUPPORTED;  // the distributed path is fp32 / fp64 only
   const int GM = ctx->GM, GK = ctx->GK;
   std::vector<int> rounds;
   st = dist_round_plan(M, N, P, Q, GM, GK, &rounds, nullptr);

@@ -1707,6 +1707,213 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
   }
 }
 
+// ------------------------------------------------------------------ fp32 chunk pairs, 3xTF32 tensor cores (v8)
+//
+// NEXT-4 (reported separately from the fp32 CUDA-core numbers): the v6 sandwich for P = 32 fp32 on the
+// legacy warp MMA (mma.sync m16n8k8 TF32, SASS HMMA; measured 275 TF/s vs 74 TF/s FFMA2,
+// profiles/r01_microbench_mma.jsonl) with the 3xTF32 split x = hi + lo per operand and
+// acc += a_lo b_hi + a_hi b_lo + a_hi b_hi (fp32 accumulation): products keep ~22 significant bits,
+// well inside the fp32 parity bar, and small-integer data stays bit-exact (lo = 0).  A warp owns a
+// chunk: GEMM1 = X . F1 (A = X rows of the TMA tile, B = F1^T rows), Z^T written in place; GEMM2 =
+// F2^T . Z (A = F2^T rows, B = Z^T rows), OUT written in place; every operand is a [32][32] matrix
+// with 128-byte rows and the 128B swizzle, so all fragment gathers are conflict free.  Factor hi/lo
+// splits are computed once per CTA.  Store warps as in v6.
+__device__ __forceinline__ uint32_t sw32(uint32_t r, uint32_t c) {  // [32][32] fp32, 128B swizzle
+  return r * 128u + ((c * 4u) ^ ((r & 7u) << 4));
+}
+
+template <int NCW, int NSW>
+__global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_tf32x3_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                              const FusedArgs a) {
+  constexpr int P = 32, C = P * P, LINE = 32;
+  constexpr uint32_t CE = C * 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  unsigned char *FT = base + (size_t)a.stages * a.stage_bytes;  // [4][32][32] tf32: F1T hi, F1T lo, F2T hi, F2T lo
+  uint64_t *full = reinterpret_cast<uint64_t *>(FT + 4 * CE);
+  uint64_t *cdone = full + a.stages, *empty = cdone + a.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  {
+    const float *F1 = reinterpret_cast<const float *>(a.F[0]);
+    const float *F2 = reinterpret_cast<const float *>(a.F[1]);
+    for (int i = tid; i < C; i += (NCW + NSW) * 32) {
+      const uint32_t r = (uint32_t)i / P, c = (uint32_t)i % P;
+      uint32_t hi, lo;
+      tf32_split(F1[i], hi, lo);  // F1[p = r][q1 = c] -> F1T[c][r]
+      *reinterpret_cast<uint32_t *>(FT + sw32(c, r)) = hi;
+      *reinterpret_cast<uint32_t *>(FT + CE + sw32(c, r)) = lo;
+      tf32_split(F2[i], hi, lo);  // F2[s = r][q2 = c] -> F2T[c][r]
+      *reinterpret_cast<uint32_t *>(FT + 2 * CE + sw32(c, r)) = hi;
+      *reinterpret_cast<uint32_t *>(FT + 3 * CE + sw32(c, r)) = lo;
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < a.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], a.R * 32);  // one arrival per lane per chunk
+      mbar_init(&empty[s], NSW * 32);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % a.stages;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * a.stage_bytes;
+    mbar_arrive_expect_tx(&full[st], a.tile_bytes);
+    const int line0 = cb * (a.tileK / LINE);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < a.stages; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    // one warp-level 32 x 32 x 32 product, 3xTF32: acc[mt][nt] = A[32][32] . B, with A rows and
+    // B^T rows both stored [32][32] swizzled; A split on the fly (xsplit) or pre-split (a_hi/a_lo)
+    auto gemm = [&](const unsigned char *Ah, const unsigned char *Al, bool asplit, const unsigned char *Bh,
+                    const unsigned char *Bl, bool bsplit, float (&acc)[2][4][4]) {
+#pragma unroll
+      for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.f;
+#pragma unroll 2
+      for (int k0 = 0; k0 < P; k0 += 8) {
+        uint32_t ah[2][4], al[2][4], bh[4][2], bl[4][2];
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t r = (uint32_t)(mt * 16 + g + 8 * (e & 1)), c = (uint32_t)(k0 + t + 4 * (e >> 1));
+            if (asplit) {
+              tf32_split(*reinterpret_cast<const float *>(Ah + sw32(r, c)), ah[mt][e], al[mt][e]);
+            } else {
+              ah[mt][e] = *reinterpret_cast<const uint32_t *>(Ah + sw32(r, c));
+              al[mt][e] = *reinterpret_cast<const uint32_t *>(Al + sw32(r, c));
+            }
+          }
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const uint32_t r = (uint32_t)(nt * 8 + g), c = (uint32_t)(k0 + t + 4 * e);
+            if (bsplit) {
+              tf32_split(*reinterpret_cast<const float *>(Bh + sw32(r, c)), bh[nt][e], bl[nt][e]);
+            } else {
+              bh[nt][e] = *reinterpret_cast<const uint32_t *>(Bh + sw32(r, c));
+              bl[nt][e] = *reinterpret_cast<const uint32_t *>(Bl + sw32(r, c));
+            }
+          }
+        // the three products of the split, small terms first; 8 independent accumulators per term
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[mt][nt], al[mt], bh[nt][0], bh[nt][1]);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[mt][nt], ah[mt], bl[nt][0], bl[nt][1]);
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt) mma_tf32(acc[mt][nt], ah[mt], bh[nt][0], bh[nt][1]);
+      }
+    };
+    for (int it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
+      unsigned char *buf = base + (size_t)st * a.stage_bytes;
+      for (int gg = warp; gg < a.R; gg += NCW) {
+        unsigned char *ch = buf + (uint32_t)gg * CE;
+        const uint32_t gx = pipe_gx<8, 4>((uint32_t)gg);
+        float acc[2][4][4];
+        // GEMM1: Z[s][q1] = sum_p X[s][p] F1[p][q1]  (A = X rows, B^T = F1T rows)
+        gemm(ch, nullptr, true, FT, FT + CE, false, acc);
+        __syncwarp();
+        // Z^T[q1][s] in place (B^T operand of GEMM2)
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const uint32_t s = (uint32_t)(mt * 16 + g + 8 * (e >> 1)), q1 = (uint32_t)(nt * 8 + 2 * t + (e & 1));
+              *reinterpret_cast<float *>(ch + sw32(q1, s)) = acc[mt][nt][e];
+            }
+        __syncwarp();
+        // GEMM2: OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]  (A = F2T rows, B^T = Z^T rows)
+        gemm(FT + 2 * CE, FT + 3 * CE, false, ch, nullptr, true, acc);
+        __syncwarp();
+        // OUT[q2][q1] in place, chunk-XOR'd for the store warps' chunk-fastest reads
+#pragma unroll
+        for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const uint32_t q2 = (uint32_t)(mt * 16 + g + 8 * v), q1 = (uint32_t)(nt * 8 + 2 * t);
+              *reinterpret_cast<float2 *>(ch + (swz128(q2 * 128u + q1 * 4u) ^ gx)) =
+                  make_float2(acc[mt][nt][2 * v], acc[mt][nt][2 * v + 1]);
+            }
+        __syncwarp();
+        mbar_arrive(&cdone[st]);  // every lane: R * 32 arrivals per tile
+      }
+    }
+  } else {
+    // ---------------- store warps: chunk-fastest stream-out (as v6), Y[row][u*(W/C) + cb*R + g]
+    const int sw = warp - NCW;
+    float *Y = reinterpret_cast<float *>(a.Y);
+    const int gl = lane & 7, uq = lane >> 3;
+    for (int it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      const uint32_t par = (uint32_t)((it / a.stages) & 1);
+      mbar_wait_sleep(&cdone[st], par);
+      const unsigned char *buf = base + (size_t)st * a.stage_bytes;
+      const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
+      for (int oct = 0; oct < a.R / 8; ++oct) {
+        const uint32_t gg = (uint32_t)(oct * 8 + gl);
+        const uint32_t gx = pipe_gx<8, 4>(gg);
+        const unsigned char *ch = buf + gg * CE;
+        const int64_t gcol = (int64_t)cbk * a.R + gg;
+        if (rb < a.M && gcol < a.WC) {
+          float *yg = Y + (int64_t)rb * a.Wout + gcol;
+          const int64_t wc = a.WC;
+#pragma unroll 2
+          for (int u16 = sw; u16 < C / 16; u16 += NSW) {
+            const uint32_t u = (uint32_t)(u16 * 16 + uq * 4);
+            const float4 v = *reinterpret_cast<const float4 *>(ch + (swz128(u * 4u) ^ gx));
+            float *p = yg + (int64_t)u * wc;
+            p[0] = v.x;
+            p[wc] = v.y;
+            p[2 * wc] = v.z;
+            p[3 * wc] = v.w;
+          }
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&empty[st]);
+      if (sw == 0) {
+        if (lane == 0) {
+          mbar_wait_sleep(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + a.stages);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ instances
 
 const FusedInstance kInstances[] = {
@@ -1737,6 +1944,9 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 16, 512, 2, 6, 0}, {KRON_F32, 32, 256, 1, 6, 0},
     // v7: fp64 64 x 32 factor pairs on DMMA (one chunk of 4096 per tile): id 33
     {KRON_F64, 64, 64, 1, 7, 0},
+    // v8: fp32 P = 32 pairs, 3xTF32 tensor-core mode (KRON_F32_3XTF32 only): id 34
+    // (16-chunk tiles: 64-byte output runs)
+    {KRON_F32, 32, 512, 1, 8, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1748,6 +1958,7 @@ Kernel4Fn instance_kernel4(int i) {
   switch (i) {
     case 30: return kron_fused_dmma2_kernel<8, 4>;
     case 33: return kron_fused_dmma2g_kernel<8, 4>;
+    case 34: return kron_fused_tf32x3_kernel<8, 4>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -1953,8 +2164,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.M = M;
   size_t smem;
   int threads = inst.NT;
-  if (inst.warp == 5) {
-    smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
+  if (inst.warp == 5 || inst.warp == 8) {
+    smem = 1024 + (size_t)a.stages * a.stage_bytes + (inst.warp == 8 ? 4 : 2) * (size_t)pp.P * pp.P * es +
+           24 * (size_t)a.stages;
     threads = 32 * (8 + 4);
   } else if (inst.warp == 6) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
@@ -1968,7 +2180,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
   }
-  if (inst.warp == 3 || inst.warp == 5) {
+  if (inst.warp == 3 || inst.warp == 5 || inst.warp == 8) {
     Kernel4Fn k4 = instance_kernel4(pp.variant);
     const int slots = kernel_slots((const void *)k4, threads, smem);
     if (slots < 1) return (int)cudaErrorInvalidConfiguration;

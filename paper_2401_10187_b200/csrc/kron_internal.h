@@ -50,7 +50,7 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0xFFu;     // allowed fused kernel families (bit = FusedInstance::warp)
+  unsigned kinds = 0x1FFu;     // allowed fused kernel families (bit = FusedInstance::warp)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool operator==(const PlanPolicy &o) const { return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma; }
 };

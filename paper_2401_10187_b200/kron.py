@@ -76,10 +76,18 @@ def _check(rc: int, what: str) -> None:
         raise KronError(rc, what)
 
 
-def dtype_code(dtype) -> int:
+MODES = {None: None, "fp32": None, "3xtf32": 2}
+
+
+def dtype_code(dtype, mode=None) -> int:
+    """C-ABI dtype: 0 float32, 1 float64, 2 float32 data in the 3xTF32 tensor-core mode (mode="3xtf32")."""
     s = str(dtype)
+    if mode not in MODES:
+        raise ValueError(f"unknown mode {mode!r} (None or '3xtf32')")
     if s.endswith("float32"):
-        return 0
+        return 2 if MODES[mode] == 2 else 0
+    if mode is not None and MODES[mode] is not None:
+        raise ValueError("the 3xTF32 mode applies to float32 data only")
     if s.endswith("float64"):
         return 1
     raise TypeError(f"Kron-Matmul supports float32 and float64, got {dtype}")
@@ -97,15 +105,15 @@ def _stream_ptr(stream) -> int:
     return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
 
 
-def workspace_size(M: int, P, Q, dtype) -> int:
+def workspace_size(M: int, P, Q, dtype, mode=None) -> int:
     Pa, Qa = _shape_arrays(P, Q)
     out = ctypes.c_size_t()
-    _check(_lib.kron_matmul_workspace_size(M, len(P), Pa, Qa, dtype_code(dtype), ctypes.byref(out)),
+    _check(_lib.kron_matmul_workspace_size(M, len(P), Pa, Qa, dtype_code(dtype, mode), ctypes.byref(out)),
            "kron_matmul_workspace_size")
     return int(out.value)
 
 
-def plan_describe(M: int, P, Q, dtype):
+def plan_describe(M: int, P, Q, dtype, mode=None):
     """[(first factor (1-based), number fused, kernel family)] of the pass plan kron_matmul uses."""
     Pa, Qa = _shape_arrays(P, Q)
     cap = 64
@@ -113,27 +121,27 @@ def plan_describe(M: int, P, Q, dtype):
     first = (ctypes.c_int32 * cap)()
     nf = (ctypes.c_int32 * cap)()
     kind = (ctypes.c_int32 * cap)()
-    _check(_lib.kron_plan_describe(M, len(P), Pa, Qa, dtype_code(dtype), cap, ctypes.byref(n), first, nf, kind),
+    _check(_lib.kron_plan_describe(M, len(P), Pa, Qa, dtype_code(dtype, mode), cap, ctypes.byref(n), first, nf, kind),
            "kron_plan_describe")
     return [(first[i], nf[i], KIND_NAMES[kind[i]]) for i in range(n.value)]
 
 
-def plan_kernels(M: int, P, Q, dtype):
+def plan_kernels(M: int, P, Q, dtype, mode=None):
     """Kernel (family) name of every pass of the plan kron_matmul uses."""
     Pa, Qa = _shape_arrays(P, Q)
     out = []
-    for i in range(len(plan_describe(M, P, Q, dtype))):
+    for i in range(len(plan_describe(M, P, Q, dtype, mode))):
         buf = ctypes.create_string_buffer(64)
-        _check(_lib.kron_plan_kernel(M, len(P), Pa, Qa, dtype_code(dtype), i, buf, 64), "kron_plan_kernel")
+        _check(_lib.kron_plan_kernel(M, len(P), Pa, Qa, dtype_code(dtype, mode), i, buf, 64), "kron_plan_kernel")
         out.append(buf.value.decode())
     return out
 
 
-def plan_cost(M: int, P, Q, dtype):
+def plan_cost(M: int, P, Q, dtype, mode=None):
     """(algorithmic HBM bytes, FLOPs) of the plan."""
     Pa, Qa = _shape_arrays(P, Q)
     b, f = ctypes.c_double(), ctypes.c_double()
-    _check(_lib.kron_plan_cost(M, len(P), Pa, Qa, dtype_code(dtype), ctypes.byref(b), ctypes.byref(f)),
+    _check(_lib.kron_plan_cost(M, len(P), Pa, Qa, dtype_code(dtype, mode), ctypes.byref(b), ctypes.byref(f)),
            "kron_plan_cost")
     return b.value, f.value
 
@@ -173,8 +181,9 @@ def _prep(X, Fs):
     return P, Q
 
 
-def matmul(X, Fs, out=None, stream=None):
-    """Y = X · (F^1 ⊗ … ⊗ F^N) on the current (or given) CUDA stream via kron_matmul()."""
+def matmul(X, Fs, out=None, stream=None, mode=None):
+    """Y = X · (F^1 ⊗ … ⊗ F^N) on the current (or given) CUDA stream via kron_matmul().
+    mode="3xtf32": float32 data in the separately reported 3xTF32 tensor-core mode."""
     import torch
     P, Q = _prep(X, Fs)
     L = 1
@@ -184,24 +193,24 @@ def matmul(X, Fs, out=None, stream=None):
         out = torch.empty((X.shape[0], L), dtype=X.dtype, device=X.device)
     Pa, Qa = _shape_arrays(P, Q)
     Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
-    _check(_lib.kron_matmul(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype),
+    _check(_lib.kron_matmul(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype, mode),
                             _stream_ptr(stream)), "kron_matmul")
     return out
 
 
-def matmul_ws(X, Fs, out, workspace, stream=None):
+def matmul_ws(X, Fs, out, workspace, stream=None, mode=None):
     """kron_matmul_ws(): caller-owned output and workspace (a uint8 CUDA tensor, or None if 0 bytes)."""
     P, Q = _prep(X, Fs)
     Pa, Qa = _shape_arrays(P, Q)
     Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
     wptr = workspace.data_ptr() if workspace is not None else None
     wbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
-    _check(_lib.kron_matmul_ws(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype),
+    _check(_lib.kron_matmul_ws(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype, mode),
                                wptr, wbytes, _stream_ptr(stream)), "kron_matmul_ws")
     return out
 
 
-def matmul_ws_events(X, Fs, out, workspace, events, stream=None):
+def matmul_ws_events(X, Fs, out, workspace, events, stream=None, mode=None):
     """kron_matmul_ws_events(): like matmul_ws, recording events[i] (raw cudaEvent_t handles) before
     pass i and events[npasses] after the last pass, for per-kernel timing."""
     P, Q = _prep(X, Fs)
@@ -211,12 +220,12 @@ def matmul_ws_events(X, Fs, out, workspace, events, stream=None):
     wptr = workspace.data_ptr() if workspace is not None else None
     wbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
     _check(_lib.kron_matmul_ws_events(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(),
-                                      dtype_code(X.dtype), wptr, wbytes, Ev, len(events), _stream_ptr(stream)),
+                                      dtype_code(X.dtype, mode), wptr, wbytes, Ev, len(events), _stream_ptr(stream)),
            "kron_matmul_ws_events")
     return out
 
 
-def autotune(X, Fs, out=None, reps: int = 3, stream=None):
+def autotune(X, Fs, out=None, reps: int = 3, stream=None, mode=None):
     """kron_autotune(): time every candidate plan on these buffers, install the fastest for this
     (device, M, shapes, dtype).  Returns (Y, number of candidates, best ms)."""
     import torch
@@ -229,15 +238,15 @@ def autotune(X, Fs, out=None, reps: int = 3, stream=None):
     Pa, Qa = _shape_arrays(P, Q)
     Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
     n, ms = ctypes.c_int32(), ctypes.c_float()
-    _check(_lib.kron_autotune(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype),
+    _check(_lib.kron_autotune(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype, mode),
                               reps, _stream_ptr(stream), ctypes.byref(n), ctypes.byref(ms)), "kron_autotune")
     return out, n.value, ms.value
 
 
-def autotune_candidates(M: int, P, Q, dtype) -> int:
+def autotune_candidates(M: int, P, Q, dtype, mode=None) -> int:
     Pa, Qa = _shape_arrays(P, Q)
     n = ctypes.c_int32()
-    _check(_lib.kron_autotune_candidates(M, len(P), Pa, Qa, dtype_code(dtype), ctypes.byref(n)),
+    _check(_lib.kron_autotune_candidates(M, len(P), Pa, Qa, dtype_code(dtype, mode), ctypes.byref(n)),
            "kron_autotune_candidates")
     return n.value
 

@@ -176,3 +176,14 @@ def test_plan_kernels(kron):
     Pa = (ctypes.c_int32 * 2)(4, 4)
     buf = ctypes.create_string_buffer(8)
     assert lib.kron_plan_kernel(16, 2, Pa, Pa, 0, 5, buf, 8) == 1   # no such pass
+
+
+def test_tf32x3_mode_plan(kron):
+    # the 3xTF32 mode (dtype code 2) changes only the P = 32 fp32 pairs; fp64 data rejects the mode
+    assert kron.plan_kernels(1024, [32] * 4, [32] * 4, "float32", "3xtf32") == ["kron_fused_tf32x3_kernel"] * 2
+    assert kron.plan_kernels(1024, [8] * 6, [8] * 6, "float32", "3xtf32") == ["kron_fused_pipe_kernel"] * 2
+    assert kron.workspace_size(1024, [32] * 4, [32] * 4, "float32", "3xtf32") == \
+        kron.workspace_size(1024, [32] * 4, [32] * 4, "float32")
+    with pytest.raises(ValueError):
+        kron.dtype_code("float64", "3xtf32")
+    assert _call(kron, 4, [2, 2], [2, 2], dtype=3) == 1   # unknown dtype code

@@ -210,3 +210,46 @@ def test_autotuned_plan_parity(kron, cuda_device, M, P, Q, dt):
     assert np.array_equal(Y.cpu().numpy(), ref)
     assert np.array_equal(run(kron, X, Fs, cuda_device), ref)
     kron.plan_cache_clear()
+
+
+# ------------------------------------------------------------------ 3xTF32 tensor-core mode (NEXT-4)
+
+TF32X3 = [
+    (40, [32] * 4, [32] * 4),   # two P = 32 pairs on the tensor cores
+    (9, [32] * 3, [32] * 3),    # pair + single factor (CUDA cores)
+    (3, [16, 32, 32], [16, 32, 32]),
+]
+
+
+@pytest.mark.parametrize("M,P,Q", TF32X3)
+def test_tf32x3_mode_parity(kron, cuda_device, M, P, Q):
+    # small integers are exact in TF32 (lo = 0) and every partial sum is an exact fp32 integer -> bit
+    # exact; U[0,1) data stays within the fp32 bar (the split keeps ~22-bit products)
+    import torch
+    for mode, seed_off in (("int1", 11), ("urand", 12)):
+        X, Fs = case(M, P, Q, np.float32, mode, seed_off)
+        ref = oracle.alg1(X, Fs)
+        Y = kron.matmul(to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs], mode="3xtf32")
+        torch.cuda.synchronize()
+        Y = Y.cpu().numpy()
+        if mode == "int1":
+            assert np.array_equal(Y, ref.astype(np.float32))
+        else:
+            assert rel_err(Y, ref) <= TOL[np.float32]
+    assert "kron_fused_tf32x3_kernel" in kron.plan_kernels(M, P, Q, "float32", "3xtf32")
+
+
+@pytest.mark.slow
+def test_tf32x3_full_size_sampled_rows(kron, cuda_device):
+    import torch
+    M, P, seed = 1024, [32] * 4, synth.SEED_BASE + 2
+    K = 32 ** 4
+    X = torch.empty((M, K), dtype=torch.float32, device=cuda_device)
+    synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", np.float32)
+    Fs_h = synth.factors(P, P, seed, "urand", np.float32)
+    Y = kron.matmul(X, [to_dev(f, cuda_device) for f in Fs_h], mode="3xtf32")
+    rows = synth.row_subset(M, extra=12)
+    Ys = Y[torch.from_numpy(rows).to(cuda_device)].cpu().numpy()
+    del X, Y
+    ref = oracle.alg1(synth.rows_of(rows, K, seed, 0, "urand"), Fs_h)
+    assert rel_err(Ys, ref) <= TOL[np.float32]
