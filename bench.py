@@ -273,6 +273,20 @@ def run_sweep(args):
             fl = flops_of(M, P, Q)
             b_alg, _ = kron.plan_cost(M, P, Q, tdt)
             line.update({"ms": round(ms, 5), "gflops": round(fl / ms / 1e6, 2), "hbm_gbs": round(b_alg / ms / 1e6, 1)})
+            # the same problem replayed as a CUDA graph (kron_graph_*): launch-bound shapes drop the
+            # per-call host cost (argument checks, plan lookup, tensor-map encodes, launches)
+            g = kron.Graph(X, Fs, Y, work)
+            for _ in range(args.warmup):
+                g.launch()
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(args.steps):
+                g.launch()
+            e1.record()
+            torch.cuda.synchronize()
+            gms = e0.elapsed_time(e1) / args.steps
+            g.close()
+            line.update({"graph_ms": round(gms, 5), "graph_gflops": round(fl / gms / 1e6, 2)})
             print(json.dumps(line), flush=True)
             del X, Y, work, Fs
             torch.cuda.empty_cache()

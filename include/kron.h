@@ -96,6 +96,19 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
                                  kron_dtype_t dtype, int32_t cap, int32_t *npasses, int32_t *first,
                                  int32_t *nfactors, int32_t *kind);
 
+/* CUDA-graph form of kron_matmul_ws for repeated calls on the same buffers (small, launch-bound
+ * problems: the paper's Table 4 shapes).  kron_graph_create captures the plan's kernel launches for
+ * these exact device pointers (X, F[i], Y, workspace; contents may change between launches, the
+ * pointers may not) into an instantiated graph; kron_graph_launch enqueues one Kron-Matmul on `stream`
+ * at graph-replay cost; kron_graph_destroy frees it.  Same argument rules as kron_matmul_ws; M = 0 is
+ * KRON_ERR_INVALID_ARG here (nothing to capture).  The graph owns no device memory. */
+typedef struct kron_graph_s kron_graph_t;
+kron_status_t kron_graph_create(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                                const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                                size_t workspace_bytes, kron_graph_t **graph);
+kron_status_t kron_graph_launch(kron_graph_t *graph, void *stream);
+kron_status_t kron_graph_destroy(kron_graph_t *graph);
+
 /* Autotuning ("performs auto-tuning over a range of tile size parameter values for the
  * given shape ... find the kernel with the least execution time").  Candidate plans (fusion group
  * caps x kernel-family choices x fp64 DMMA on/off; duplicates removed) are each run once untimed and

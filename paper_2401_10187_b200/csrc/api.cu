@@ -452,6 +452,66 @@ kron_status_t kron_matmul_ws(int64_t M, int32_t N, const int32_t *P, const int32
   return run_plan(*plan, X, F, Y, workspace, stream);
 }
 
+struct kron_graph_s {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+kron_status_t kron_graph_create(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                                const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
+                                size_t workspace_bytes, kron_graph_t **out) {
+  if (!out) return KRON_ERR_INVALID_ARG;
+  *out = nullptr;
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_ERR_INVALID_ARG;
+  if (!X || !F || !Y) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  std::shared_ptr<const Plan> plan;
+  st = cached_plan(M, N, P, Q, (int)dtype, &plan);
+  if (st != KRON_OK) return st;
+  const size_t need = ws_bytes_of(*plan);
+  if (need > 0 && (!workspace || workspace_bytes < need)) return KRON_ERR_SHAPE;
+  // capture the plan's launches on a private stream (thread-local capture mode: other threads' CUDA
+  // calls are unaffected); one-time launch bookkeeping (function attributes) happens during capture
+  cudaStream_t cs;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess)
+    return cuda_fail((int)cudaGetLastError(), "graph capture stream");
+  auto *g = new kron_graph_s();
+  cudaError_t e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) {
+    st = run_plan(*plan, X, F, Y, workspace, cs);
+    e = cudaStreamEndCapture(cs, &g->graph);
+    if (st == KRON_OK && e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  }
+  cudaStreamDestroy(cs);
+  if (st == KRON_OK && e != cudaSuccess) st = cuda_fail((int)e, "graph capture / instantiate");
+  if (st != KRON_OK) {
+    cudaGetLastError();
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+    return st;
+  }
+  *out = g;
+  return KRON_OK;
+}
+
+kron_status_t kron_graph_launch(kron_graph_t *g, void *stream) {
+  if (!g || !g->exec) return KRON_ERR_INVALID_ARG;
+  const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
+  return e == cudaSuccess ? KRON_OK : cuda_fail((int)e, "graph launch");
+}
+
+kron_status_t kron_graph_destroy(kron_graph_t *g) {
+  if (!g) return KRON_OK;
+  if (g->exec) cudaGraphExecDestroy(g->exec);
+  if (g->graph) cudaGraphDestroy(g->graph);
+  delete g;
+  return KRON_OK;
+}
+
 kron_status_t kron_matmul_ws_events(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
                                     const void *const *F, void *Y, kron_dtype_t dtype, void *workspace,
                                     size_t workspace_bytes, void *const *events, int32_t nevents, void *stream) {

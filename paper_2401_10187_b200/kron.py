@@ -61,6 +61,14 @@ _lib.kron_plan_kernel.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, 
 _lib.kron_plan_cache_clear.restype = ctypes.c_int
 _lib.kron_plan_cache_clear.argtypes = []
 
+_lib.kron_graph_create.restype = ctypes.c_int
+_lib.kron_graph_create.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
+                                   ctypes.c_int, ctypes.c_void_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]
+_lib.kron_graph_launch.restype = ctypes.c_int
+_lib.kron_graph_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+_lib.kron_graph_destroy.restype = ctypes.c_int
+_lib.kron_graph_destroy.argtypes = [ctypes.c_void_p]
+
 KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm"}
 
 
@@ -253,6 +261,34 @@ def autotune_candidates(M: int, P, Q, dtype, mode=None) -> int:
 
 def plan_cache_clear() -> None:
     _check(_lib.kron_plan_cache_clear(), "kron_plan_cache_clear")
+
+
+class Graph:
+    """kron_graph_create(): the plan's launches for these exact tensors captured in a CUDA graph;
+    launch() enqueues one Kron-Matmul at graph-replay cost (contents may change, storage may not)."""
+
+    def __init__(self, X, Fs, out, workspace, mode=None):
+        P, Q = _prep(X, Fs)
+        Pa, Qa = _shape_arrays(P, Q)
+        Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
+        wptr = workspace.data_ptr() if workspace is not None else None
+        wbytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+        h = ctypes.c_void_p()
+        _check(_lib.kron_graph_create(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(),
+                                      dtype_code(X.dtype, mode), wptr, wbytes, ctypes.byref(h)), "kron_graph_create")
+        self.handle = h.value
+        self._keep = (X, list(Fs), out, workspace)  # the captured pointers must stay alive
+
+    def launch(self, stream=None):
+        _check(_lib.kron_graph_launch(self.handle, _stream_ptr(stream)), "kron_graph_launch")
+
+    def close(self):
+        if getattr(self, "handle", None):
+            _lib.kron_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
 
 
 def raw_lib():

@@ -187,3 +187,14 @@ def test_tf32x3_mode_plan(kron):
     with pytest.raises(ValueError):
         kron.dtype_code("float64", "3xtf32")
     assert _call(kron, 4, [2, 2], [2, 2], dtype=3) == 1   # unknown dtype code
+
+
+def test_graph_argument_errors(kron):
+    # kron_graph_create validates synchronously (nothing is captured on bad arguments)
+    lib = kron.raw_lib()
+    Pa = (ctypes.c_int32 * 2)(4, 4)
+    h = ctypes.c_void_p()
+    assert lib.kron_graph_create(4, 2, Pa, Pa, None, None, None, 0, None, 0, ctypes.byref(h)) == 1
+    assert lib.kron_graph_create(0, 2, Pa, Pa, 1, None, 1, 0, None, 0, ctypes.byref(h)) == 1  # M = 0
+    assert lib.kron_graph_launch(None, None) == 1
+    assert lib.kron_graph_destroy(None) == 0

@@ -253,3 +253,35 @@ def test_tf32x3_full_size_sampled_rows(kron, cuda_device):
     del X, Y
     ref = oracle.alg1(synth.rows_of(rows, K, seed, 0, "urand"), Fs_h)
     assert rel_err(Ys, ref) <= TOL[np.float32]
+
+
+@pytest.mark.parametrize("M,P,Q,dt", [(20, [2] * 7, [2] * 7, np.float32), (16, [8] * 3, [8] * 3, np.float64),
+                                      (40, [32] * 4, [32] * 4, np.float32), (4, [64] * 3, [32] * 3, np.float64)])
+def test_graph_replay(kron, cuda_device, M, P, Q, dt):
+    # kron_graph_*: the captured plan replays bit-identically, and reads the buffers' current contents
+    import torch
+    X, Fs = case(M, P, Q, dt, "urand", 21)
+    Xd, Fd = to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs]
+    tdt = Xd.dtype
+    ws = torch.empty(max(kron.workspace_size(M, P, Q, tdt), 1), dtype=torch.uint8, device=cuda_device)
+    Y1 = torch.empty((M, int(np.prod(Q))), dtype=tdt, device=cuda_device)
+    Y2 = torch.empty_like(Y1)
+    kron.matmul_ws(Xd, Fd, Y1, ws)
+    g = kron.Graph(Xd, Fd, Y2, ws)
+    g.launch()
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    X2, _ = case(M, P, Q, dt, "int" if dt == np.float64 else "int1", 22)
+    Xd.copy_(torch.from_numpy(X2))
+    for _ in range(3):
+        g.launch()
+    torch.cuda.synchronize()
+    g.close()
+    # integer X with U[0,1) factors is not exact; compare against the direct call on the new data
+    Y3 = torch.empty_like(Y1)
+    kron.matmul_ws(Xd, Fd, Y3, ws)
+    torch.cuda.synchronize()
+    assert torch.equal(Y2, Y3)
+    ref = oracle.alg1(X2, Fs)
+    den = oracle.alg1(np.abs(X2), [np.abs(f) for f in Fs])
+    assert float(np.max(np.abs(Y2.cpu().numpy() - ref) / np.maximum(den, 1e-300))) <= TOL[dt]
