@@ -198,3 +198,18 @@ def test_graph_argument_errors(kron):
     assert lib.kron_graph_create(0, 2, Pa, Pa, 1, None, 1, 0, None, 0, ctypes.byref(h)) == 1  # M = 0
     assert lib.kron_graph_launch(None, None) == 1
     assert lib.kron_graph_destroy(None) == 0
+
+
+def test_table4_shapes_plan_and_autotune(kron):
+    # every paper Table 4 shape (odd M, odd / mixed / non-square factors) gets a legal plan, and the
+    # autotuner has at least one candidate for it (Table 4)
+    import bench
+    for M, P, Q in bench.TABLE4:
+        for dt in ("float32", "float64"):
+            plan = kron.plan_describe(M, P, Q, dt)
+            covered = []
+            for first, nf, _ in plan:
+                covered += list(range(first, first - nf, -1))
+            assert covered == list(range(len(P), 0, -1))
+            assert kron.autotune_candidates(M, P, Q, dt) >= 1
+            assert len(kron.plan_kernels(M, P, Q, dt)) == len(plan)
