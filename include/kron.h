@@ -96,6 +96,18 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
                                  kron_dtype_t dtype, int32_t cap, int32_t *npasses, int32_t *first,
                                  int32_t *nfactors, int32_t *kind);
 
+/* Host-buffer Kron-Matmul (the end-to-end path): X, F[i] and Y are HOST pointers (page-locked memory
+ * strongly recommended: pageable memory makes the copies synchronous).  Rows are independent
+ * (Algorithm 1), so the call streams chunks of `chunk_rows` rows (0 = ~64 MB per chunk) through
+ * two device slots: the host->device copy of chunk c+1, the passes of chunk c and the device->host copy
+ * of chunk c-1 overlap on two internal copy streams and `stream`.  Device memory (factors, two slots,
+ * workspace) is allocated and freed stream-ordered.  Everything is ordered after prior work on `stream`
+ * and `stream` completes with the last copy; the call returns without synchronising (Y is valid after
+ * the stream synchronises).  Errors as kron_matmul; chunk_rows < 0 -> KRON_ERR_INVALID_ARG. */
+kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                               const void *const *F, void *Y, kron_dtype_t dtype, int64_t chunk_rows,
+                               void *stream);
+
 /* CUDA-graph form of kron_matmul_ws for repeated calls on the same buffers (small, launch-bound
  * problems: the paper's Table 4 shapes).  kron_graph_create captures the plan's kernel launches for
  * these exact device pointers (X, F[i], Y, workspace; contents may change between launches, the

@@ -556,6 +556,114 @@ kron_status_t kron_matmul(int64_t M, int32_t N, const int32_t *P, const int32_t 
   return st;
 }
 
+kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
+                               const void *const *F, void *Y, kron_dtype_t dtype, int64_t chunk_rows,
+                               void *stream) {
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  if (M == 0) return KRON_OK;
+  if (!X || !F || !Y || chunk_rows < 0) return KRON_ERR_INVALID_ARG;
+  for (int i = 0; i < N; ++i)
+    if (!F[i]) return KRON_ERR_INVALID_ARG;
+  const size_t es = (size_t)es_of((int)dtype);
+  int64_t K = 1, L = 1;
+  for (int i = 0; i < N; ++i) {
+    K *= P[i];
+    L *= Q[i];
+  }
+  // rows are independent (Alg 1): stream row chunks of ~64 MB through two device slots
+  int64_t Mc = chunk_rows;
+  if (Mc == 0) Mc = (int64_t)((64u << 20) / ((size_t)(K > L ? K : L) * es));
+  if (Mc < 1) Mc = 1;
+  if (Mc > M) Mc = M;
+  const int64_t nchunks = (M + Mc - 1) / Mc, Mt = M - (nchunks - 1) * Mc;
+  std::shared_ptr<const Plan> pc, pt;
+  if ((st = cached_plan(Mc, N, P, Q, (int)dtype, &pc)) != KRON_OK) return st;
+  if ((st = cached_plan(Mt, N, P, Q, (int)dtype, &pt)) != KRON_OK) return st;
+  const size_t wsb = std::max(ws_bytes_of(*pc), ws_bytes_of(*pt));
+  size_t fbytes = 0;
+  std::vector<size_t> foff(N);
+  for (int i = 0; i < N; ++i) {
+    foff[i] = fbytes;
+    fbytes += (((size_t)P[i] * Q[i] * es + 255) / 256) * 256;
+  }
+  const size_t xb = (size_t)Mc * K * es, yb = (size_t)Mc * L * es;
+  const size_t xs = (xb + 255) / 256 * 256, ys = (yb + 255) / 256 * 256, wss = (wsb + 255) / 256 * 256;
+  cudaStream_t sc = (cudaStream_t)stream, sin = nullptr, sout = nullptr;
+  char *dev = nullptr;
+  keep_pool_cached();
+  if (cudaMallocAsync((void **)&dev, fbytes + 2 * xs + 2 * ys + wss, sc) != cudaSuccess) {
+    cudaGetLastError();
+    return KRON_ERR_NO_MEMORY;
+  }
+  char *Fd = dev, *Xs[2] = {dev + fbytes, dev + fbytes + xs}, *Ys[2] = {dev + fbytes + 2 * xs, dev + fbytes + 2 * xs + ys};
+  char *ws = wsb ? dev + fbytes + 2 * xs + 2 * ys : nullptr;
+  cudaEvent_t ev0, evF, ev_in[2], ev_comp[2], ev_out[2];
+  cudaError_t e = cudaSuccess;
+  auto ck = [&](cudaError_t r) {
+    if (e == cudaSuccess && r != cudaSuccess) e = r;
+  };
+  ck(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking));
+  ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking));
+  ck(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+  ck(cudaEventCreateWithFlags(&evF, cudaEventDisableTiming));
+  for (int b = 0; b < 2; ++b) {
+    ck(cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming));
+    ck(cudaEventCreateWithFlags(&ev_comp[b], cudaEventDisableTiming));
+    ck(cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming));
+  }
+  if (e != cudaSuccess) {
+    cudaFreeAsync(dev, sc);
+    return cuda_fail((int)e, "host-path streams / events");
+  }
+  // the copy streams start after the caller's prior work and the allocation
+  ck(cudaEventRecord(ev0, sc));
+  ck(cudaStreamWaitEvent(sin, ev0, 0));
+  ck(cudaStreamWaitEvent(sout, ev0, 0));
+  std::vector<const void *> Fdev(N);
+  for (int i = 0; i < N; ++i) {
+    Fdev[i] = Fd + foff[i];
+    ck(cudaMemcpyAsync(Fd + foff[i], F[i], (size_t)P[i] * Q[i] * es, cudaMemcpyHostToDevice, sin));
+  }
+  ck(cudaEventRecord(evF, sin));
+  ck(cudaStreamWaitEvent(sc, evF, 0));
+  for (int64_t c = 0; c < nchunks && e == cudaSuccess && st == KRON_OK; ++c) {
+    const int b = (int)(c & 1);
+    const int64_t r0 = c * Mc, rows = c + 1 < nchunks ? Mc : Mt;
+    // H2D of chunk c once compute c-2 is done with slot b
+    if (c >= 2) ck(cudaStreamWaitEvent(sin, ev_comp[b], 0));
+    ck(cudaMemcpyAsync(Xs[b], static_cast<const char *>(X) + (size_t)r0 * K * es, (size_t)rows * K * es,
+                       cudaMemcpyHostToDevice, sin));
+    ck(cudaEventRecord(ev_in[b], sin));
+    // the passes of chunk c once its rows landed and D2H c-2 has drained slot b
+    ck(cudaStreamWaitEvent(sc, ev_in[b], 0));
+    if (c >= 2) ck(cudaStreamWaitEvent(sc, ev_out[b], 0));
+    st = run_plan(c + 1 < nchunks ? *pc : *pt, Xs[b], Fdev.data(), Ys[b], ws, sc);
+    ck(cudaEventRecord(ev_comp[b], sc));
+    // D2H of chunk c
+    ck(cudaStreamWaitEvent(sout, ev_comp[b], 0));
+    ck(cudaMemcpyAsync(static_cast<char *>(Y) + (size_t)r0 * L * es, Ys[b], (size_t)rows * L * es,
+                       cudaMemcpyDeviceToHost, sout));
+    ck(cudaEventRecord(ev_out[b], sout));
+  }
+  // the caller's stream completes with the last copies; buffers are released stream-ordered after them
+  for (int b = 0; b < 2; ++b) ck(cudaStreamWaitEvent(sc, ev_out[b], 0));
+  ck(cudaEventRecord(ev0, sin));
+  ck(cudaStreamWaitEvent(sc, ev0, 0));
+  cudaFreeAsync(dev, sc);
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(evF);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(ev_in[b]);
+    cudaEventDestroy(ev_comp[b]);
+    cudaEventDestroy(ev_out[b]);
+  }
+  cudaStreamDestroy(sin);
+  cudaStreamDestroy(sout);
+  if (st != KRON_OK) return st;
+  return e == cudaSuccess ? KRON_OK : cuda_fail((int)e, "host-path copies");
+}
+
 // Candidate plans for the autotuner: fusion-depth caps x kernel-family masks x fp64 DMMA,
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {

@@ -69,6 +69,10 @@ _lib.kron_graph_launch.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
 _lib.kron_graph_destroy.restype = ctypes.c_int
 _lib.kron_graph_destroy.argtypes = [ctypes.c_void_p]
 
+_lib.kron_matmul_host.restype = ctypes.c_int
+_lib.kron_matmul_host.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
+                                  ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]
+
 KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm"}
 
 
@@ -203,6 +207,32 @@ def matmul(X, Fs, out=None, stream=None, mode=None):
     Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
     _check(_lib.kron_matmul(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(), dtype_code(X.dtype, mode),
                             _stream_ptr(stream)), "kron_matmul")
+    return out
+
+
+def matmul_host(X, Fs, out=None, chunk_rows: int = 0, stream=None, mode=None):
+    """kron_matmul_host(): X, Fs and out are CPU tensors (pin_memory() for overlap); the library streams
+    row chunks host -> device -> host with the copies overlapping the passes.  Asynchronous on
+    `stream` (synchronise before reading `out`)."""
+    import torch
+    if X.dim() != 2 or X.is_cuda or not X.is_contiguous():
+        raise ValueError("X must be a contiguous 2-D CPU tensor")
+    P = [int(f.shape[0]) for f in Fs]
+    Q = [int(f.shape[1]) for f in Fs]
+    for f in Fs:
+        if f.is_cuda or not f.is_contiguous() or f.dtype != X.dtype or f.dim() != 2:
+            raise ValueError("factors must be contiguous 2-D CPU tensors of X's dtype")
+    K = L = 1
+    for p, q in zip(P, Q):
+        K, L = K * p, L * q
+    if X.shape[1] != K:
+        raise ValueError(f"X has {X.shape[1]} columns, prod P = {K}")
+    if out is None:
+        out = torch.empty((X.shape[0], L), dtype=X.dtype, pin_memory=X.is_pinned())
+    Pa, Qa = _shape_arrays(P, Q)
+    Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
+    _check(_lib.kron_matmul_host(X.shape[0], len(P), Pa, Qa, X.data_ptr(), Fp, out.data_ptr(),
+                                 dtype_code(X.dtype, mode), chunk_rows, _stream_ptr(stream)), "kron_matmul_host")
     return out
 
 

@@ -213,3 +213,12 @@ def test_table4_shapes_plan_and_autotune(kron):
             assert covered == list(range(len(P), 0, -1))
             assert kron.autotune_candidates(M, P, Q, dt) >= 1
             assert len(kron.plan_kernels(M, P, Q, dt)) == len(plan)
+
+
+def test_host_path_argument_errors(kron):
+    lib = kron.raw_lib()
+    Pa = (ctypes.c_int32 * 2)(4, 4)
+    assert lib.kron_matmul_host(4, 2, Pa, Pa, None, None, None, 0, 0, None) == 1     # null buffers
+    Fp = (ctypes.c_void_p * 2)(1, 1)
+    assert lib.kron_matmul_host(4, 2, Pa, Pa, 1, Fp, 1, 0, -1, None) == 1           # chunk_rows < 0
+    assert lib.kron_matmul_host(0, 2, Pa, Pa, None, None, None, 0, 0, None) == 0     # M = 0: no-op

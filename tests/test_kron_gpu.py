@@ -285,3 +285,17 @@ def test_graph_replay(kron, cuda_device, M, P, Q, dt):
     ref = oracle.alg1(X2, Fs)
     den = oracle.alg1(np.abs(X2), [np.abs(f) for f in Fs])
     assert float(np.max(np.abs(Y2.cpu().numpy() - ref) / np.maximum(den, 1e-300))) <= TOL[dt]
+
+
+@pytest.mark.parametrize("M,P,Q,dt,chunk", [(37, [8] * 4, [8] * 4, np.float32, 8), (10, [32] * 3, [32] * 3, np.float64, 3),
+                                            (9, [64] * 3, [32] * 3, np.float64, 4), (5, [3, 5], [4, 2], np.float32, 0)])
+def test_host_path(kron, cuda_device, M, P, Q, dt, chunk):
+    # kron_matmul_host: host buffers, row chunks (with a ragged tail) pipelined through two device slots
+    import torch
+    mode = "int1" if dt == np.float32 else "int"
+    X, Fs = case(M, P, Q, dt, mode, 31)
+    Xh = torch.from_numpy(X).pin_memory()
+    Fh = [torch.from_numpy(f).pin_memory() for f in Fs]
+    Y = kron.matmul_host(Xh, Fh, chunk_rows=chunk)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.numpy(), oracle.alg1(X, Fs).astype(dt))
