@@ -1919,7 +1919,9 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_tf32x3_kernel(
 const FusedInstance kInstances[] = {
     // dtype, P, NT (threads doing the last step), RS (slices per thread, last step), kind, rsw
     // v3 factor-pipelined (factors in registers): ids 0..4
-    {KRON_F32, 2, 128, 16, 2, 4}, {KRON_F32, 4, 128, 8, 2, 4}, {KRON_F32, 8, 128, 4, 2, 2},
+    // (P = 8: 32 KB tiles, so the last group's output runs are 16 chunks = 64 bytes; 16 KB tiles (32-byte
+    //  runs) measured 0.82 ms on config B vs 0.74 ms)
+    {KRON_F32, 2, 128, 16, 2, 4}, {KRON_F32, 4, 128, 8, 2, 4}, {KRON_F32, 8, 128, 8, 2, 2},
     {KRON_F64, 2, 128, 8, 2, 2},  {KRON_F64, 4, 128, 4, 2, 2},
     // v4 two-factor GEMM chunks (nf == 2 only): ids 25..26 appended at the end
     // v2 (warp-local chain): ids 5..14
