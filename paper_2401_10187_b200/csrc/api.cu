@@ -67,8 +67,8 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
   }
   if (inst.warp == 5) {
-    // DMMA chunk pairs: exactly two factors, one tile row of 4 chunks (32-byte fp64 runs)
-    if (k != 2 || tileM != 1 || R != 4 || (R * C) != E) return false;
+    // DMMA chunk pairs: exactly two factors, one tile row of 8 chunks (64-byte fp64 runs)
+    if (k != 2 || tileM != 1 || R != 8 || (R * C) != E) return false;
   }
   if (inst.warp == 2 || inst.warp == 4) {
     if (k > 3) return false;                                   // one warp group per factor

@@ -1372,14 +1372,14 @@ __device__ __forceinline__ uint32_t rowswz32(uint32_t r, uint32_t c) {  // [rows
   return line * 128u + (((c & 15u) << 3) ^ ((line & 7u) << 4));
 }
 
-// Warp-specialised: NCW compute warps (one chunk each; with NCW = 2 * CPT two groups take alternate
-// tiles so every SM sub-partition has two DMMA warps) never stop for the HBM stream-out, which NSW
+// Warp-specialised: NCW compute warps (one chunk each per tile; with NCW = 2 * CPT two groups take
+// alternate tiles; NCW = 8 gives every SM sub-partition two DMMA warps) never stop for the HBM stream-out, which NSW
 // store warps do from the finished tile while the compute warps work on the next ones (mbarriers:
 // full = TMA landed, cdone = chunks computed, empty = tile streamed out -> refill).
-template <int NCW, int NSW>
+template <int NCW, int NSW, int CPT>
 __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                              const FusedArgs a) {
-  constexpr int P = 32, C = P * P, LINE = 16, CPT = 4;  // chunks per tile
+  constexpr int P = 32, C = P * P, LINE = 16;  // CPT = chunks per tile
   static_assert(NCW % CPT == 0, "compute warps come in groups of one tile");
   constexpr uint32_t CB = C * 8;  // chunk bytes
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1939,8 +1939,9 @@ const FusedInstance kInstances[] = {
     {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
     // L2-fused pair of factor pipelines (two passes in one cooperative launch): id 29
     {KRON_F32, 8, 64, 8, 4, 2},
-    // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 128 * RS * P = 4 chunks): id 30
-    {KRON_F64, 32, 128, 1, 5, 0},
+    // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 256 * RS * P = 8 chunks = 64-byte output runs;
+    //     4-chunk tiles (32-byte runs) measured 9.42 ms on C64 vs 8.93 ms): id 30
+    {KRON_F64, 32, 256, 1, 5, 0},
     // v6: fp32 two-factor chunks, warp-specialised (tile = 8192 elements): ids 31..32
     // (P = 16: 64-chunk tiles = 256-byte output runs; P = 32: 8-chunk tiles = 32-byte runs)
     {KRON_F32, 16, 512, 2, 6, 0}, {KRON_F32, 32, 256, 1, 6, 0},
@@ -1958,7 +1959,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
-    case 30: return kron_fused_dmma2_kernel<8, 4>;
+    case 30: return kron_fused_dmma2_kernel<8, 4, 8>;
     case 33: return kron_fused_dmma2g_kernel<8, 4>;
     case 34: return kron_fused_tf32x3_kernel<8, 4>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
