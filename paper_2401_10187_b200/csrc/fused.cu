@@ -1932,7 +1932,7 @@ const FusedInstance kInstances[] = {
     // v1 (CTA-wide in-place chain, any chunk size): ids 15..24
     {KRON_F32, 2, 256, 8, 0, 0},  {KRON_F32, 4, 256, 4, 0, 0},  {KRON_F32, 8, 128, 4, 0, 0},
     {KRON_F32, 16, 256, 2, 0, 0}, {KRON_F32, 32, 128, 2, 0, 0}, {KRON_F64, 2, 256, 4, 0, 0},
-    {KRON_F64, 4, 256, 2, 0, 0},  {KRON_F64, 8, 256, 1, 0, 0},  {KRON_F64, 16, 128, 2, 0, 0},
+    {KRON_F64, 4, 256, 2, 0, 0},  {KRON_F64, 8, 256, 2, 0, 0},  {KRON_F64, 16, 128, 2, 0, 0},
     {KRON_F64, 32, 128, 1, 0, 0},
     // v4: two-factor chunk GEMMs (tile = 256 * RS * P elements = 8192)
     {KRON_F32, 16, 256, 2, 3, 0}, {KRON_F32, 32, 256, 1, 3, 0},
@@ -2003,7 +2003,7 @@ KernelFn instance_kernel(int i) {
     case 19: return kron_fused_kernel<float, 32, 2, 128>;
     case 20: return kron_fused_kernel<double, 2, 4, 256>;
     case 21: return kron_fused_kernel<double, 4, 2, 256>;
-    case 22: return kron_fused_kernel<double, 8, 1, 256>;
+    case 22: return kron_fused_kernel<double, 8, 2, 256>;
     case 23: return kron_fused_kernel<double, 16, 2, 128>;
     case 24: return kron_fused_kernel<double, 32, 1, 128>;
   }
