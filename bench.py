@@ -308,7 +308,7 @@ def run_dist(args, ws, rank, local, dev, barrier):
     if ws == 1:
         GM, GK = 1, 1
     if ws > 1:
-        ctx = kron.DistContext("nccl", GM=GM, GK=GK)
+        ctx = kron.DistContext(args.exchange, GM=GM, GK=GK)
     else:
         ctx = kron.DistContext("virtual", GM=1, GK=1)
     gm, gk = ctx.coords(rank)
@@ -319,7 +319,7 @@ def run_dist(args, ws, rank, local, dev, barrier):
                       c0=gk * Kl, ld=K)
     Fs = [torch.from_numpy(f).to(dev) for f in synth.factors(P, Q, seed, "urand", dt)]
     Y = torch.empty((Ml, L // ctx.GK), dtype=tdt, device=dev)
-    xs, ys = (X, Y) if ctx.backend == "nccl" else ([X], [Y])
+    xs, ys = (X, Y) if ctx.backend != "virtual" else ([X], [Y])
     for _ in range(args.warmup):
         kron.matmul_dist(M, xs, Fs, ctx, out=ys)
     torch.cuda.synchronize()
@@ -353,7 +353,9 @@ def run_dist(args, ws, rank, local, dev, barrier):
             "data": "synthetic (seeded counter-based U[0,1), each rank generates its own block in HBM)",
             "config": {"workload": args.config, "M": M, "P": P, "Q": Q, "grid": [ctx.GM, ctx.GK],
                        "rounds": rounds, "exchanged_values_per_step": int(sum(ledger)),
-                       "parallelism": f"Algorithm 2 grid {ctx.GM}x{ctx.GK} (rows x K), NCCL all-to-all",
+                       "parallelism": f"Algorithm 2 grid {ctx.GM}x{ctx.GK} (rows x K), " +
+                                      ("NCCL all-to-all" if args.exchange == "nccl" else
+                                       "P2P pull kernel over peer memory (CUDA IPC)"),
                        "l2": "inputs larger than L2 (no flush)"},
             "step_roofline": {"t_roof_ms_per_gpu": round(t_roof * 1e3, 4),
                               "frac": round(t_roof / (ms / args.steps / 1e3), 4)},
@@ -379,6 +381,9 @@ def main():
     ap.add_argument("--dist", action="store_true",
                     help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
                          "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="--dist exchange: ncclAlltoAll (pack / all-to-all / StoreGPUTile) or the one-kernel "
+                         "P2P pull over peer memory (NEXT-1, P:652)")
     ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
     ap.add_argument("--mode", default=None, choices=["3xtf32"],
                     help="fp32 configs only: the separately reported 3xTF32 tensor-core mode (NEXT-4)")

@@ -168,6 +168,15 @@ kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32
  *     1  virtual: ONE process drives all GM*GK ranks on the current device; the exchange is a
  *        device-to-device copy (used to test the distributed data path on a single GPU).
  *        nccl_unique_id and rank are ignored.
+ *     2  P2P (peer memory, "a single CUDA kernel ... when GPUs support P2P"): one rank per
+ *        process (`rank` = this process's rank, nccl_unique_id ignored).  Before the first call the
+ *        ranks reserve a symmetric heap (kron_dist_p2p_reserve), exchange its 64-byte CUDA IPC
+ *        handles (e.g. all_gather over a torch ProcessGroup) and map the row-group peers' heaps
+ *        (kron_dist_p2p_connect).  Each round then writes its local output into this rank's heap,
+ *        meets the row group at a device-side flag barrier, and runs ONE pull kernel that reads every
+ *        value it owns straight from the peers' heaps (NVLink / NVSwitch loads) into its StoreGPUTile
+ *        position — the pack, the all-to-all and StoreGPUTile of backend 0 in a single pass.
+ *        Ranks may share a GPU (IPC within one device), which is how it is tested on one B200.
  * GM = GK = 0 selects the grid by the paper's rule.                               */
 typedef struct kron_dist_ctx kron_dist_ctx_t;
 
@@ -179,8 +188,31 @@ kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */
 kron_status_t kron_dist_nccl_unique_id(void *out128);
 
+/* Backend 2 (P2P) symmetric heap.
+ * kron_dist_p2p_heap_bytes: heap bytes kron_matmul_dist needs for this problem on a {GM,GK} grid
+ *   (two halves of M/GM x max round output width / GK elements; 0 when GK = 1).  Host only.
+ * kron_dist_p2p_reserve: (re)allocates this rank's heap of `bytes` usable bytes plus a 4 KB header
+ *   (barrier flags, timeout word) with cudaMalloc on the current device, zeroes the header, and writes
+ *   its cudaIpcMemHandle_t (64 bytes) to `ipc_handle_out`.  Collective in effect: every rank of the
+ *   context calls it, and no rank may still be using the previous heaps (synchronize + barrier first).
+ *   Errors: wrong backend / null -> KRON_ERR_INVALID_ARG; allocation -> KRON_ERR_NO_MEMORY;
+ *   IPC export -> KRON_ERR_CUDA.
+ * kron_dist_p2p_connect: `ipc_handles` = world_size x 64 bytes in rank order (all ranks' handles);
+ *   opens the heaps of this rank's row-group peers (cudaIpcOpenMemHandle, lazy peer access).
+ *   Errors: no heap reserved -> KRON_ERR_INVALID_ARG; IPC open failure -> KRON_ERR_CUDA.
+ * kron_matmul_dist on backend 2 returns KRON_ERR_INVALID_ARG before connect and KRON_ERR_NO_MEMORY
+ *   when the heap is smaller than kron_dist_p2p_heap_bytes.  Calls on one context must be issued in
+ *   stream order on each rank (heap halves and barrier epochs continue across calls).
+ * kron_dist_p2p_timeouts: synchronously reads how many barrier waits gave up (~20 s bound instead of
+ *   hanging the device when a peer never arrives); 0 in a healthy run.                          */
+kron_status_t kron_dist_p2p_heap_bytes(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                       int32_t GM, int32_t GK, size_t *bytes);
+kron_status_t kron_dist_p2p_reserve(kron_dist_ctx_t *ctx, size_t bytes, void *ipc_handle_out);
+kron_status_t kron_dist_p2p_connect(kron_dist_ctx_t *ctx, const void *ipc_handles);
+kron_status_t kron_dist_p2p_timeouts(kron_dist_ctx_t *ctx, uint32_t *count);
+
 /* Collective over the context's ranks: every rank calls it with identical M, N, P, Q, dtype.
- * NCCL backend: X_local / Y_local are this rank's blocks.
+ * NCCL and P2P backends: X_local / Y_local are this rank's blocks.
  * Virtual backend: X_local / Y_local are host arrays of GM*GK device pointers, one per rank.
  * dtype KRON_F32 or KRON_F64 (KRON_F32_3XTF32 -> KRON_ERR_UNSUPPORTED).
  * Errors: GM !| M, GK !| K, GK !| L or no legal round plan -> KRON_ERR_DIST_LAYOUT (shape-only,

@@ -268,7 +268,8 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
     const int inst_t = (tf32x3 && p == q && allowed(8)) ? fused_find(dtype, p, 8) : -1;
-    const int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
+    int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
+    if (inst_s >= 0 && getenv("KRON_V6_SMALL") && dtype == KRON_F32 && p == 16) inst_s = 35;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;

@@ -20,6 +20,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -163,6 +164,109 @@ int launch_store_gpu_tile(int dtype, const void *recv, void *out, int64_t rows, 
   return (int)cudaGetLastError();
 }
 
+// ------------------------------------------------------------------ P2P exchange over peer memory (NEXT-1)
+//
+// The paper notes that lines 676-690 of Algorithm 2 can run as ONE kernel when the GPUs can access each
+// other's memory.  Backend 2 does that: every rank's round output lives in a symmetric heap
+// (cudaMalloc + CUDA IPC, mapped by the peers of its row group over NVLink / NVSwitch), and after a
+// device-side flag barrier each rank PULLS its values straight from the peers' heaps into their
+// StoreGPUTile position of its next-round block (or of Y_local after the last round):
+//
+//   dst[m][(e*GK + src)*rho + t] = out_src[m][me*B + e*rho + t]          (B = W'/GK, t < rho)
+//
+// which is the pack kernel, the all-to-all and the StoreGPUTile kernel of backend 0 in one pass (one
+// HBM read at the source, one write at the destination, no send / receive buffers).  The round outputs
+// alternate between two halves of the heap, so one barrier per round suffices: when a rank passes the
+// barrier of round j every peer has finished its round j-1 pulls, which is the half round j+1 rewrites.
+
+constexpr int kMaxPeers = 64;
+constexpr size_t kP2PHeader = 4096;       // heap header: u64 flag per row-group peer, then the timeout word
+constexpr size_t kP2PTimeoutOff = 8 * kMaxPeers;
+struct PeerPtrs {
+  const char *p[kMaxPeers];
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Row-group barrier: lane i signals peer i (flag slot `me` of its heap) with the epoch, then waits until
+// peer i has signalled this rank.  The wait is bounded (~`spin_ns`): on timeout it counts the miss in
+// the heap's timeout word (kron_dist_p2p_timeouts) instead of hanging the device.
+__global__ void p2p_barrier_kernel(PeerPtrs heaps, unsigned long long *my_flags, int GK, int me,
+                                   unsigned long long epoch, unsigned *timeouts, long long spin_ns) {
+  const int i = threadIdx.x;
+  if (i >= GK || i == me) return;
+  __threadfence_system();  // this rank's earlier kernels (its round output) before the signal
+  st_release_sys(reinterpret_cast<unsigned long long *>(const_cast<char *>(heaps.p[i])) + me, epoch);
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (ld_acquire_sys(my_flags + i) < epoch) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > spin_ns) {
+      atomicAdd(timeouts, 1u);
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+// Pull + StoreGPUTile.  V = elements per vector (16 bytes when rho*es and the offsets allow, else 1).
+template <typename T, int V>
+__global__ void __launch_bounds__(256) p2p_pull_kernel(PeerPtrs outs, T *__restrict__ dst, int64_t rows, int64_t Wl,
+                                                       int64_t rho, int GK, int me) {
+  using Vec = typename std::conditional<V == 1, T, uint4>::type;
+  const int64_t B = Wl / GK, rv = rho / V, n = rows * (Wl / V);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    Vec v[4];
+    int64_t di[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // four independent remote loads in flight per thread
+      const int64_t i = i0 + u * stride;
+      di[u] = -1;
+      if (i < n) {
+        const int64_t m = i / (Wl / V), c = i - m * (Wl / V);
+        const int64_t run = c / rv, t = c - run * rv;
+        const int64_t e = run / GK, src = run - e * GK;
+        const Vec *s = reinterpret_cast<const Vec *>(outs.p[src]) + m * (Wl / V) + me * (B / V) + e * rv + t;
+        v[u] = *s;
+        di[u] = i;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (di[u] >= 0) reinterpret_cast<Vec *>(dst)[di[u]] = v[u];
+  }
+}
+
+int launch_p2p_pull(int dtype, const PeerPtrs &outs, void *dst, int64_t rows, int64_t Wl, int64_t rho, int GK, int me,
+                    cudaStream_t s) {
+  const int64_t n = rows * Wl;
+  if (n == 0) return 0;
+  const int es = dtype == KRON_F32 ? 4 : 8;
+  const int V = 16 / es;
+  bool vec = (rho * es) % 16 == 0 && (Wl * es) % 16 == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+  for (int g = 0; g < GK; ++g) vec &= (reinterpret_cast<uintptr_t>(outs.p[g]) & 15) == 0;
+  int64_t blocks = (n / (vec ? V : 1) + 1023) / 1024;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  if (dtype == KRON_F32) {
+    if (vec) p2p_pull_kernel<float, 4><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+    else p2p_pull_kernel<float, 1><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+  } else {
+    if (vec) p2p_pull_kernel<double, 2><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+    else p2p_pull_kernel<double, 1><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+  }
+  return (int)cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ NCCL via dlopen
 
 struct NcclApi {
@@ -214,9 +318,16 @@ const NcclApi &nccl() {
 using namespace kron;
 
 struct kron_dist_ctx {
-  int backend = 0;  // 0 NCCL, 1 virtual
+  int backend = 0;  // 0 NCCL, 1 virtual, 2 P2P (peer memory)
   int world = 1, rank = 0, GM = 1, GK = 1, gM = 0, gK = 0;
   ncclComm_t world_comm = nullptr, row_comm = nullptr;
+  // backend 2: symmetric heap = [flags: u64 per row-group peer | timeout word] [out half 0] [out half 1]
+  char *heap = nullptr;
+  size_t heap_bytes = 0;                 // usable bytes (both halves)
+  char *peer_heap[kron::kMaxPeers] = {};  // row-group peers' heaps (index gK; own heap at this->gK)
+  bool connected = false;
+  unsigned long long epoch = 0;  // barrier epoch (identical on every rank: calls are collective)
+  unsigned parity = 0;           // which heap half the next round writes
 };
 
 namespace kron {
@@ -278,7 +389,7 @@ kron_status_t kron_dist_nccl_unique_id(void *out128) {
 
 kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, int32_t world_size, int32_t rank,
                                    int32_t GM, int32_t GK, kron_dist_ctx_t **out) {
-  if (!out || world_size < 1 || (backend != 0 && backend != 1)) return KRON_ERR_INVALID_ARG;
+  if (!out || world_size < 1 || backend < 0 || backend > 2) return KRON_ERR_INVALID_ARG;
   *out = nullptr;
   if (GM == 0 && GK == 0) {
     kron_status_t st = grid_rule(world_size, &GM, &GK);
@@ -312,8 +423,28 @@ kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, 
       return KRON_ERR_NCCL;
     }
   }
+  if (backend == 2) {
+    if (rank < 0 || rank >= world_size || GK > kMaxPeers) {
+      delete ctx;
+      return KRON_ERR_INVALID_ARG;
+    }
+    ctx->rank = rank;
+    ctx->gM = rank / GK;
+    ctx->gK = rank % GK;
+  }
   *out = ctx;
   return KRON_OK;
+}
+
+static void p2p_release(kron_dist_ctx_t *ctx) {
+  for (int g = 0; g < ctx->GK && g < kMaxPeers; ++g) {
+    if (ctx->peer_heap[g] && ctx->peer_heap[g] != ctx->heap) cudaIpcCloseMemHandle(ctx->peer_heap[g]);
+    ctx->peer_heap[g] = nullptr;
+  }
+  if (ctx->heap) cudaFree(ctx->heap);
+  ctx->heap = nullptr;
+  ctx->heap_bytes = 0;
+  ctx->connected = false;
 }
 
 kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx) {
@@ -323,7 +454,84 @@ kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx) {
     if (ctx->row_comm) api.CommDestroy(ctx->row_comm);
     if (ctx->world_comm) api.CommDestroy(ctx->world_comm);
   }
+  if (ctx->backend == 2) p2p_release(ctx);
   delete ctx;
+  return KRON_OK;
+}
+
+kron_status_t kron_dist_p2p_heap_bytes(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                       int32_t GM, int32_t GK, size_t *bytes) {
+  if (!bytes) return KRON_ERR_INVALID_ARG;
+  kron_status_t st = validate(M, N, P, Q, (int)dtype);
+  if (st != KRON_OK) return st;
+  std::vector<int> rounds;
+  st = dist_round_plan(M, N, P, Q, GM, GK, &rounds, nullptr);
+  if (st != KRON_OK) return st;
+  std::vector<int64_t> W(N + 1);
+  W[N] = 1;
+  for (int i = 0; i < N; ++i) W[N] *= P[i];
+  for (int f = N; f >= 1; --f) W[f - 1] = W[f] / P[f - 1] * Q[f - 1];
+  int64_t mw = 0;
+  int f = N;
+  for (int k : rounds) {
+    f -= k;
+    mw = std::max(mw, W[f] / GK);
+  }
+  const int64_t half = ((M / GM) * mw * (dtype == KRON_F64 ? 8 : 4) + 255) / 256 * 256;
+  *bytes = GK > 1 ? (size_t)(2 * half) : 0;
+  return KRON_OK;
+}
+
+kron_status_t kron_dist_p2p_reserve(kron_dist_ctx_t *ctx, size_t bytes, void *ipc_handle_out) {
+  if (!ctx || ctx->backend != 2 || !ipc_handle_out) return KRON_ERR_INVALID_ARG;
+  p2p_release(ctx);
+  bytes = (bytes + 511) / 512 * 512;
+  if (cudaMalloc(&ctx->heap, kP2PHeader + bytes) != cudaSuccess) {
+    cudaGetLastError();
+    ctx->heap = nullptr;
+    return KRON_ERR_NO_MEMORY;
+  }
+  cudaIpcMemHandle_t h;
+  if (cudaMemset(ctx->heap, 0, kP2PHeader) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess ||
+      cudaIpcGetMemHandle(&h, ctx->heap) != cudaSuccess) {
+    cudaGetLastError();
+    p2p_release(ctx);
+    return KRON_ERR_CUDA;
+  }
+  memcpy(ipc_handle_out, &h, sizeof(h));
+  ctx->heap_bytes = bytes;
+  ctx->epoch = 0;
+  ctx->parity = 0;
+  return KRON_OK;
+}
+
+kron_status_t kron_dist_p2p_connect(kron_dist_ctx_t *ctx, const void *ipc_handles) {
+  if (!ctx || ctx->backend != 2 || !ctx->heap || !ipc_handles) return KRON_ERR_INVALID_ARG;
+  for (int g = 0; g < ctx->GK; ++g) {
+    if (g == ctx->gK) {
+      ctx->peer_heap[g] = ctx->heap;
+      continue;
+    }
+    if (ctx->peer_heap[g]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, static_cast<const char *>(ipc_handles) + (size_t)(ctx->gM * ctx->GK + g) * sizeof(h), sizeof(h));
+    void *p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      return KRON_ERR_CUDA;
+    }
+    ctx->peer_heap[g] = static_cast<char *>(p);
+  }
+  ctx->connected = true;
+  return KRON_OK;
+}
+
+kron_status_t kron_dist_p2p_timeouts(kron_dist_ctx_t *ctx, uint32_t *count) {
+  if (!ctx || ctx->backend != 2 || !count) return KRON_ERR_INVALID_ARG;
+  *count = 0;
+  if (!ctx->heap) return KRON_OK;
+  if (cudaMemcpy(count, ctx->heap + kP2PTimeoutOff, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return KRON_ERR_CUDA;
   return KRON_OK;
 }
 
@@ -405,13 +613,26 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     }
   }
   const size_t buf_bytes = (size_t)Ml * max_w * es;
+  const bool p2p = ctx->backend == 2;
+  size_t half = 0;
+  if (p2p) {
+    // the round outputs live in the symmetric heap (two halves); see kron_dist_p2p_heap_bytes
+    size_t need = 0;
+    st = kron_dist_p2p_heap_bytes(M, N, P, Q, dtype, GM, GK, &need);
+    if (st != KRON_OK) return st;
+    if (!ctx->connected) return KRON_ERR_INVALID_ARG;
+    if (need > ctx->heap_bytes) return KRON_ERR_NO_MEMORY;
+    half = need / 2;
+  }
   std::vector<RankBufs> bufs(nranks);
   bool oom = false;
   for (int r = 0; r < nranks; ++r) {
     oom |= cudaMallocAsync(&bufs[r].cur, buf_bytes, s) != cudaSuccess;
-    oom |= cudaMallocAsync(&bufs[r].out, buf_bytes, s) != cudaSuccess;
-    oom |= cudaMallocAsync(&bufs[r].send, buf_bytes, s) != cudaSuccess;
-    oom |= cudaMallocAsync(&bufs[r].recv, buf_bytes, s) != cudaSuccess;
+    if (!p2p) {
+      oom |= cudaMallocAsync(&bufs[r].out, buf_bytes, s) != cudaSuccess;
+      oom |= cudaMallocAsync(&bufs[r].send, buf_bytes, s) != cudaSuccess;
+      oom |= cudaMallocAsync(&bufs[r].recv, buf_bytes, s) != cudaSuccess;
+    }
     if (ws_max) oom |= cudaMallocAsync(&bufs[r].ws, ws_max, s) != cudaSuccess;
   }
   auto free_all = [&] {
@@ -432,6 +653,28 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     const bool last = j + 1 == rounds.size();
     const int64_t B = R.wl_out / GK;       // values per row sent to each peer
     const size_t blk = (size_t)Ml * B;     // values per peer
+    if (p2p) {
+      // lines 670-674 into this rank's heap half, barrier, then lines 676-690 + 685 as one pull kernel
+      const size_t off = kP2PHeader + (size_t)ctx->parity * half;
+      const void *in = j == 0 ? Xv[0] : bufs[0].cur;
+      st = plan_run(R.plan, in, Fj, ctx->heap + off, bufs[0].ws, stream);
+      if (st != KRON_OK) break;
+      PeerPtrs heaps{}, outs{};
+      for (int g = 0; g < GK; ++g) {
+        heaps.p[g] = ctx->peer_heap[g];
+        outs.p[g] = ctx->peer_heap[g] + off;
+      }
+      const unsigned long long ep = ++ctx->epoch;
+      p2p_barrier_kernel<<<1, 64, 0, s>>>(heaps, reinterpret_cast<unsigned long long *>(ctx->heap), GK, ctx->gK, ep,
+                                          reinterpret_cast<unsigned *>(ctx->heap + kP2PTimeoutOff),
+                                          (long long)20 * 1000 * 1000 * 1000);
+      if (cudaGetLastError() != cudaSuccess) st = KRON_ERR_CUDA;
+      void *dst = last ? Yv[0] : bufs[0].cur;
+      if (st == KRON_OK && launch_p2p_pull((int)dtype, outs, dst, Ml, R.wl_out, R.rho, GK, ctx->gK, s) != 0)
+        st = KRON_ERR_CUDA;
+      ctx->parity ^= 1u;
+      continue;
+    }
     // lines 670-674: local sliced multiplies; then pack the destination-major send buffer
     for (int r = 0; r < nranks && st == KRON_OK; ++r) {
       const void *in = j == 0 ? Xv[r] : bufs[r].cur;

@@ -1950,6 +1950,8 @@ const FusedInstance kInstances[] = {
     // v8: fp32 P = 32 pairs, 3xTF32 tensor-core mode (KRON_F32_3XTF32 only): id 34
     // (16-chunk tiles: 64-byte output runs)
     {KRON_F32, 32, 512, 1, 8, 0},
+    // v6 P = 16 with 32-chunk tiles (128-byte runs, twice the ring stages): id 35 (autotuner candidate)
+    {KRON_F32, 16, 256, 2, 6, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1986,6 +1988,7 @@ KernelFn instance_kernel(int i) {
   switch (i) {
     case 31: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4>;
     case 32: return kron_fused_gemm2ws_kernel<32, 12, 4, 8, 4>;
+    case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
     case 7: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;

@@ -332,6 +332,15 @@ _lib.kron_dist_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.kron_dist_ctx_create.restype = ctypes.c_int
 _lib.kron_dist_ctx_create.argtypes = [ctypes.c_int32, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                       ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)]
+_lib.kron_dist_p2p_heap_bytes.restype = ctypes.c_int
+_lib.kron_dist_p2p_heap_bytes.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, ctypes.c_int32,
+                                          ctypes.c_int32, ctypes.POINTER(ctypes.c_size_t)]
+_lib.kron_dist_p2p_reserve.restype = ctypes.c_int
+_lib.kron_dist_p2p_reserve.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p]
+_lib.kron_dist_p2p_connect.restype = ctypes.c_int
+_lib.kron_dist_p2p_connect.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
+_lib.kron_dist_p2p_timeouts.restype = ctypes.c_int
+_lib.kron_dist_p2p_timeouts.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32)]
 _lib.kron_dist_ctx_destroy.restype = ctypes.c_int
 _lib.kron_dist_ctx_destroy.argtypes = [ctypes.c_void_p]
 _lib.kron_dist_ctx_grid.restype = ctypes.c_int
@@ -361,6 +370,14 @@ class DistContext:
             uid = ctypes.create_string_buffer(obj[0], 128)
             _check(_lib.kron_dist_ctx_create(0, uid, world_size, rank, GM, GK, ctypes.byref(self.handle)),
                    "kron_dist_ctx_create")
+        elif backend == "p2p":
+            # peer-memory exchange (backend 2): the symmetric heap is reserved lazily by matmul_dist,
+            # collectively, with its CUDA IPC handles all-gathered over `pg` (plumbing only)
+            import torch.distributed as dist
+            world_size = dist.get_world_size(pg) if world_size is None else world_size
+            rank = dist.get_rank(pg) if rank is None else rank
+            _check(_lib.kron_dist_ctx_create(2, None, world_size, rank, GM, GK, ctypes.byref(self.handle)),
+                   "kron_dist_ctx_create")
         elif backend == "virtual":
             if world_size is None:
                 world_size = GM * GK
@@ -370,9 +387,33 @@ class DistContext:
         else:
             raise ValueError(backend)
         self.backend, self.rank, self.world_size = backend, rank, world_size
+        self.pg, self.heap_bytes = pg, 0
         gm, gk = ctypes.c_int32(), ctypes.c_int32()
         _check(_lib.kron_dist_ctx_grid(self.handle, ctypes.byref(gm), ctypes.byref(gk)), "kron_dist_ctx_grid")
         self.GM, self.GK = gm.value, gk.value
+
+    def ensure_heap(self, nbytes: int) -> None:
+        """P2P backend: (re)reserve the symmetric heap if it is smaller than `nbytes` and map the peers'
+        heaps.  Collective: every rank calls it with the same size (matmul_dist does)."""
+        if nbytes <= self.heap_bytes:
+            return
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        dist.barrier(group=self.pg)  # nobody still reads the old heaps
+        h = ctypes.create_string_buffer(64)
+        _check(_lib.kron_dist_p2p_reserve(self.handle, nbytes, h), "kron_dist_p2p_reserve")
+        allh = [None] * self.world_size
+        dist.all_gather_object(allh, bytes(h.raw), group=self.pg)
+        buf = ctypes.create_string_buffer(b"".join(allh), 64 * self.world_size)
+        _check(_lib.kron_dist_p2p_connect(self.handle, buf), "kron_dist_p2p_connect")
+        self.heap_bytes = nbytes
+
+    def timeouts(self) -> int:
+        """P2P backend: barrier waits that gave up (0 in a healthy run; synchronizes)."""
+        c = ctypes.c_uint32()
+        _check(_lib.kron_dist_p2p_timeouts(self.handle, ctypes.byref(c)), "kron_dist_p2p_timeouts")
+        return c.value
 
     def coords(self, rank=None):
         r = self.rank if rank is None else rank
@@ -411,6 +452,11 @@ def matmul_dist(M, X_local, Fs, ctx: DistContext, out=None, stream=None):
         outs = [torch.empty(shape, dtype=xs[0].dtype, device=xs[0].device) for _ in xs]
     else:
         outs = out if isinstance(out, (list, tuple)) else [out]
+    if ctx.backend == "p2p":
+        need = ctypes.c_size_t()
+        _check(_lib.kron_dist_p2p_heap_bytes(M, len(P), Pa, Qa, dtype_code(xs[0].dtype), ctx.GM, ctx.GK,
+                                             ctypes.byref(need)), "kron_dist_p2p_heap_bytes")
+        ctx.ensure_heap(need.value)
     if ctx.backend == "virtual":
         xp = (ctypes.c_void_p * len(xs))(*[x.data_ptr() for x in xs])
         yp = (ctypes.c_void_p * len(outs))(*[y.data_ptr() for y in outs])
