@@ -34,9 +34,23 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   int64_t C = 1;
   for (int i = 0; i < k; ++i) C *= p;
   const int64_t E = inst.elems();
-  if (W % line || W % C || C > E) return false;
+  if (W % line || W % C || (C > E && inst.warp != 10)) return false;
   const int64_t WC = W / C;
   if ((WC * es) % 16) return false;
+  if (inst.warp == 10) {
+    // v9 cluster pair: three factors, 8-chunk tiles split 4 + 4 over two CTAs (32-byte runs)
+    if (k != 3 || p != 16 || inst.dtype != KRON_F32 || W % (8 * C)) return false;
+    pp->kind = KIND_FUSED;
+    pp->nf = 3;
+    pp->P = pp->Q = p;
+    pp->C = pp->Qc = C;
+    pp->R = 8;
+    pp->tileK = 4 * C;  // per CTA
+    pp->tileM = 1;
+    pp->stages = 3;
+    pp->nout = 0;
+    return true;
+  }
   int64_t R = E / C;
   if (R > WC) R = WC;
   if (R > 256) R = 256;
@@ -268,8 +282,9 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
     const int inst_t = (tf32x3 && p == q && allowed(8)) ? fused_find(dtype, p, 8) : -1;
+    const int inst_3 = (p == q && allowed(10)) ? fused_find(dtype, p, 10) : -1;
     int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
-    if (inst_s >= 0 && getenv("KRON_V6_SMALL") && dtype == KRON_F32 && p == 16) inst_s = 35;
+    if (inst_s >= 0 && policy.short_tiles && dtype == KRON_F32 && p == 16) inst_s = 35;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;
@@ -304,6 +319,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_3 >= 0 && fused_geometry(fused_instance(inst_3), k, W, Mp, pp)) return inst_3;
         if (inst_t >= 0 && fused_geometry(fused_instance(inst_t), k, W, Mp, pp)) return inst_t;
         if (inst_d >= 0 && fused_geometry(fused_instance(inst_d), k, W, Mp, pp)) return inst_d;
         if (inst_s >= 0 && fused_geometry(fused_instance(inst_s), k, W, Mp, pp)) return inst_s;
@@ -669,8 +685,8 @@ kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x1FFu;
-  const unsigned kinds[] = {all, all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
+  const unsigned all = 0x7FFu;
+  const unsigned kinds[] = {all, all & ~(1u << 10), all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
                             all & ~((1u << 3) | (1u << 5) | (1u << 6) | (1u << 7)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
   std::vector<Plan> cands;
@@ -684,6 +700,7 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
     }
     return true;
   };
+  for (int st = 0; st <= 1; ++st)
   for (int dm = 1; dm >= 0; --dm)
     for (unsigned km : kinds)
       for (int cap : caps) {
@@ -691,6 +708,7 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
         pol.kcap = cap;
         pol.kinds = km;
         pol.dmma = dm == 1;
+        pol.short_tiles = st == 1;
         Plan pl;
         if (make_plan(M, N, P, Q, dtype, &pl, 1, pol) != KRON_OK) continue;
         bool dup = false;
@@ -804,9 +822,10 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
   } else if (pp.kind == KIND_FUSED) {
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
-                                  "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel", "kron_fused_tf32x3_kernel"};
+                                  "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel", "kron_fused_tf32x3_kernel",
+                                  "kron_fused_kernel",         "kron_fused_gemm3c_kernel"};
     const int w = fused_instance(pp.variant).warp;
-    k = (w >= 0 && w < 9) ? names[w] : "kron_fused_kernel";
+    k = (w >= 0 && w < 11) ? names[w] : "kron_fused_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

@@ -1128,7 +1128,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
 // full = landed, cdone = computed, empty = streamed out -> refill).  Output runs are R*4 bytes; the
 // measured write rate of such runs (tools/microbench_scatter.cu: 2.9 TB/s at 32 B, 4.5 TB/s at 128 B,
 // profiles/r01_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
-template <int P, int NCW, int RM, int RN, int VA>
+template <int P, int NCW, int RM, int RN, int VA, int KU = 1>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                               const __grid_constant__ CUtensorMap tm_out,
                                                                               const FusedArgs a) {
@@ -1196,7 +1196,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
       for (int i = 0; i < RM; ++i)
 #pragma unroll
         for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
-#pragma unroll 1
+#pragma unroll KU
       for (int k0 = 0; k0 < P; k0 += 8) {
         uint32_t ab[RM];
 #pragma unroll
@@ -1357,6 +1357,274 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
       }
     }
   }
+}
+
+// ------------------------------------------------------------------ fp32 16x16 factor triples on a CTA pair (v9)
+//
+// NEXT-2 (cluster / DSMEM fusion, "Fused <= floor(log_P TileK)" with the tile spanning a cluster):
+// three 16 x 16 fp32 factors per pass, chunk C = 4096.  32-byte output runs need 8 chunks = 128 KB per
+// tile, which leaves no room for a TMA ring in one CTA; here a cluster of two CTAs owns the 8-chunk tile
+// (4 chunks = 64 KB each, three-stage ring each) and the stream-out gathers every 32-byte run from both
+// CTAs' shared memory (lane pairs: one 16-byte half local, one over DSMEM), so each store instruction
+// writes whole sectors (16-byte runs measured ~1.3 TB/s, tools/microbench.cu).
+//   phase 1 (per 256-element subchunk [d2][d3], the v6 sandwich): S = F2^T . (X . F1), in place;
+//   phase 2 (per 4096-chunk [d1][256]):  OUT[q3][col] = sum_d1 F3[d1][q3] . S[d1][col], in place by
+//   64-column blocks (a warp reads and writes the same locations);
+//   composite column u = q3*256 + q2*16 + q1 -> Y[row][u*(W/C) + 8*group + 4*rank + t], t < 4.
+// Barriers per stage: full (TMA), p1[chunk] (phase 1 of that chunk done), cdone (phase 2 of the tile done
+// in BOTH CTAs: every phase-2 lane arrives locally and, release.cluster, on the peer), empty (this CTA's
+// store lanes + the peer's last store warp, release.cluster: both CTAs' reads of this stage are done).
+// compute-sanitizer racecheck / synccheck / memcheck clean (tools/sanitize.py).
+template <int NCW>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
+    kron_fused_gemm3c_kernel(const __grid_constant__ CUtensorMap tm_in, const FusedArgs a) {
+  using T = float;
+  constexpr int P = 16, RM = 4, RN = 8, VA = 4, ES = 4, PE = P * ES, C1 = P * P;
+  constexpr uint32_t CE = C1 * ES;                // subchunk bytes (1 KB)
+  constexpr int NSW = 4, L1 = (P / RM) * (P / RN), CPG = 32 / L1;
+  constexpr int SUB = 64;                         // subchunks per CTA tile (4 chunks of 4096)
+  constexpr int U1 = SUB / CPG, U2 = 16, UPT = U1 + U2;
+  constexpr uint32_t TB = SUB * CE;               // 64 KB per CTA tile
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = a.stages;
+  T *F1s = reinterpret_cast<T *>(base + (size_t)S * TB);     // [p][q1], plain
+  unsigned char *F2Ts = reinterpret_cast<unsigned char *>(F1s + C1);  // [q2][p], 128B-swizzled
+  unsigned char *F3Ts = F2Ts + CE;                                    // [q3][p], 128B-swizzled
+  uint64_t *full = reinterpret_cast<uint64_t *>(F3Ts + CE);
+  uint64_t *p1 = full + S, *cdone = p1 + 4 * S, *empty = cdone + S;
+  unsigned *scnt = reinterpret_cast<unsigned *>(empty + S);  // store warps done with the stage
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
+  const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int64_t groups = a.tiles_k;  // 8-chunk groups per row
+
+  {
+    const T *F1 = reinterpret_cast<const T *>(a.F[0]);
+    const T *F2 = reinterpret_cast<const T *>(a.F[1]);
+    const T *F3 = reinterpret_cast<const T *>(a.F[2]);
+    for (int i = tid; i < C1; i += (NCW + NSW) * 32) {
+      const uint32_t r = (uint32_t)i / P, c = (uint32_t)i % P;
+      F1s[i] = F1[i];
+      *reinterpret_cast<T *>(F2Ts + swz128(c * PE + r * ES)) = F2[i];
+      *reinterpret_cast<T *>(F3Ts + swz128(c * PE + r * ES)) = F3[i];
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      for (int t = 0; t < 4; ++t) mbar_init(&p1[4 * s + t], (CPG == 4 ? 4 : 16 / CPG) * 32);
+      mbar_init(&cdone[s], 2 * U2 * 32);  // every phase-2 lane of this CTA and of the peer
+      mbar_init(&empty[s], NSW * 32 + 1);  // every store lane of this CTA + the peer's last store warp
+      scnt[s] = 0;
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  cluster_sync_all();  // barriers initialised in both CTAs before any remote arrive
+  auto issue_load = [&](int it) {
+    const int64_t tile = cid + (int64_t)it * ncl;
+    if (tile >= a.ntiles) return;
+    const int st = it % S;
+    const int rb = (int)(tile / groups), gj = (int)(tile - (int64_t)rb * groups);
+    unsigned char *dst = base + (size_t)st * TB;
+    mbar_arrive_expect_tx(&full[st], TB);
+    const int line0 = (gj * 8 + (int)rank * 4) * (4096 / 32);
+    for (int b = 0; b < a.nbox; ++b)
+      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < S; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    // one warp-level P x P x P product with 128B-swizzled A rows arow[] (k in blocks of 8)
+    auto gemm = [&](const unsigned char *A, const uint32_t (&arow)[RM], auto loadB, T (&acc)[RM][RN]) {
+#pragma unroll
+      for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
+#pragma unroll 2
+      for (int k0 = 0; k0 < P; k0 += 8) {
+        uint32_t ab[RM];
+#pragma unroll
+        for (int i = 0; i < RM; ++i) ab[i] = arow[i] ^ (uint32_t)(k0 * ES);
+#pragma unroll
+        for (int kk = 0; kk < 8; kk += VA) {
+          T xa[RM][VA];
+#pragma unroll
+          for (int i = 0; i < RM; ++i) {
+            const float4 v = *reinterpret_cast<const float4 *>(A + (ab[i] ^ (uint32_t)(kk * ES)));
+            xa[i][0] = v.x; xa[i][1] = v.y; xa[i][2] = v.z; xa[i][3] = v.w;
+          }
+#pragma unroll
+          for (int e = 0; e < VA; ++e) {
+            T f[RN];
+            loadB(k0, kk + e, f);
+#pragma unroll
+            for (int i = 0; i < RM; ++i) {
+              const float2 xx = make_float2(xa[i][e], xa[i][e]);
+#pragma unroll
+              for (int j = 0; j < RN; j += 2) {
+                const float2 r2 = __ffma2_rn(xx, make_float2(f[j], f[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+                acc[i][j] = r2.x;
+                acc[i][j + 1] = r2.y;
+              }
+            }
+          }
+        }
+      }
+    };
+    // phase-1 lane roles (as v6): c1 = subchunk of the unit, sg = row group, q1g = column group
+    const int c1 = lane / L1, tau = lane % L1;
+    const int sg = tau % (P / RM), q1g = tau / (P / RM);
+    uint32_t arow[RM];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) arow[i] = swz128((uint32_t)(sg + (P / RM) * i) * PE);
+    // phase-2 lane roles: rows q3 = sg2 + 4i, 8 columns cg*8 .. +8 of the unit's 64-column block
+    // (a quarter-warp = 8 lanes of one q3 row: its eight 16-byte column granules are distinct banks)
+    const int sg2 = lane / 8, cg = lane % 8;
+    uint32_t arow2[RM];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) arow2[i] = swz128((uint32_t)(sg2 + 4 * i) * PE);
+
+    for (int un = warp;; un += NCW) {
+      const int it = un / UPT, wu = un % UPT;
+      const int64_t tile = cid + (int64_t)it * ncl;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      unsigned char *buf = base + (size_t)st * TB;
+      T acc[RM][RN];
+      // unit order inside a tile (groups of 4 units): phase 1 of chunks 0, 1, 2, phase 2 of chunk 0, phase 1
+      // of chunk 3, phase 2 of chunks 1, 2, 3 — a chunk's phase 2 starts about one wave of units after its
+      // phase 1, so the p1 waits rarely block
+      constexpr unsigned kOrder = 0x76534210u;  // nibble i = (phase 2 ? 4 : 0) + chunk of group i
+      const int og = (int)((kOrder >> (4 * (wu / 4))) & 15u);
+      const int w = og < 4 ? og * 4 + wu % 4 : U1 + (og - 4) * 4 + wu % 4;
+      if (w < U1) {
+        mbar_wait(&full[st], par);
+        const uint32_t gg = (uint32_t)(w * CPG + c1);
+        unsigned char *ch = buf + gg * CE;
+        const uint32_t gx = pipe_gx<8, 4>(gg);
+        gemm(ch, arow, [&](int k0, int kk, T (&f)[RN]) {  // Z = X . F1
+          const T *fr = F1s + (k0 + kk) * P + q1g * RN;
+#pragma unroll
+          for (int j = 0; j < RN; j += 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(fr + j);
+            f[j] = v.x; f[j + 1] = v.y; f[j + 2] = v.z; f[j + 3] = v.w;
+          }
+        }, acc);
+        __syncwarp();
+        auto put = [&]() {
+#pragma unroll
+          for (int i = 0; i < RM; ++i)
+#pragma unroll
+            for (int j = 0; j < RN; j += 4)
+              *reinterpret_cast<float4 *>(ch + ((arow[i] ^ (uint32_t)((q1g * RN + j) * ES)) ^ gx)) =
+                  make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        };
+        put();
+        __syncwarp();
+        const uint32_t Kq = (uint32_t)(q1g * RN * ES) ^ gx;
+        gemm(F2Ts, arow, [&](int k0, int kk, T (&f)[RN]) {  // S = F2^T . Z
+          const int line0 = (k0 * PE) >> 7, line = (kk * PE) >> 7, a4 = ((kk * PE) & 127) >> 4;
+          const uint32_t Kb = Kq ^ ((uint32_t)(line0 & 7) << 4);
+          const unsigned char *zb = ch + (line0 + line) * 128;
+#pragma unroll
+          for (int j = 0; j < RN; j += 4) {
+            const uint32_t v = (uint32_t)(a4 ^ (j / 4) ^ (line & 7));
+            const float4 t = *reinterpret_cast<const float4 *>(zb + (Kb ^ (v << 4)));
+            f[j] = t.x; f[j + 1] = t.y; f[j + 2] = t.z; f[j + 3] = t.w;
+          }
+        }, acc);
+        __syncwarp();
+        put();
+        __syncwarp();
+        mbar_arrive(&p1[4 * st + (int)(gg / 16)]);
+      } else {
+        const int w2 = w - U1, t = w2 / 4, cb = w2 % 4;
+        mbar_wait(&p1[4 * st + t], par);
+        const uint32_t cofs = swz128((uint32_t)(cb * 64 + cg * 8) * ES);
+        unsigned char *cbase = buf + (uint32_t)(t * 16) * CE;
+        gemm(F3Ts, arow2, [&](int k0, int kk, T (&f)[RN]) {  // OUT = F3^T . S over the 16 subchunks
+          // subchunk t*16 + k: its granule XOR depends on k mod 8 only (t*16 = 0 mod 8)
+          const uint32_t o = (uint32_t)(k0 + kk) * CE + (cofs ^ pipe_gx<8, 4>((uint32_t)(k0 + kk)));
+          const float4 v0 = *reinterpret_cast<const float4 *>(cbase + o);
+          const float4 v1 = *reinterpret_cast<const float4 *>(cbase + (o ^ 16u));
+          f[0] = v0.x; f[1] = v0.y; f[2] = v0.z; f[3] = v0.w;
+          f[4] = v1.x; f[5] = v1.y; f[6] = v1.z; f[7] = v1.w;
+        }, acc);
+        __syncwarp();  // every lane's reads of the column block are done before it is overwritten
+#pragma unroll
+        for (int i = 0; i < RM; ++i) {
+          const uint32_t o = (uint32_t)(sg2 + 4 * i) * CE + (cofs ^ pipe_gx<8, 4>((uint32_t)(sg2 + 4 * i)));
+          *reinterpret_cast<float4 *>(cbase + o) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+          *reinterpret_cast<float4 *>(cbase + (o ^ 16u)) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        }
+        __syncwarp();
+        // the last phase-2 unit of the tile publishes it to both CTAs (one cluster-scope release per tile,
+        // from a warp with no global stores in flight)
+        // every lane publishes its own writes to both CTAs' store warps (release at cluster scope; a compute
+        // warp has no global stores in flight, so the fence is cheap here)
+        mbar_arrive(&cdone[st]);
+        mbar_arrive_cluster(&cdone[st], peer);
+      }
+    }
+  } else {
+    // ---------------- store warps: lane pair (i, h) gathers the 8-element run of composite column u from
+    // CTA h's four chunks (h = this CTA: local; else DSMEM) and writes its 16-byte half of the 32-byte run
+    const int sw = warp - NCW;
+    T *Y = reinterpret_cast<T *>(a.Y);
+    const int li = lane >> 1, h = lane & 1;
+    for (int it = 0;; ++it) {
+      const int64_t tile = cid + (int64_t)it * ncl;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      // both CTAs' tiles are computed (the peer's writes were released at cluster scope before its arrive)
+      mbar_wait_cluster(&cdone[st], par);
+      const int rb = (int)(tile / groups), gj = (int)(tile - (int64_t)rb * groups);
+      const uint32_t sb = mapa_shared(smem_u32(base + (size_t)st * TB), (uint32_t)h);
+      if (rb < a.M) {
+        T *yb = Y + (int64_t)rb * a.Wout + (int64_t)gj * 8 + h * 4;
+        const int64_t wc = a.WC;
+        // lane pair (li, h): four consecutive composite columns u0 .. u0+3 (one 16-byte granule per chunk)
+#pragma unroll 2
+        for (int ub = (int)rank * 2048 + sw * 64; ub < (int)rank * 2048 + 2048; ub += NSW * 64) {
+          const uint32_t u0 = (uint32_t)(ub + 4 * li), q3 = u0 >> 8;
+          const uint32_t co = swz128((u0 & 255u) * ES);
+          float4 v[4];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            const uint32_t gg = (uint32_t)(t * 16) + q3;
+            v[t] = ld_dsmem_f32x4(sb + gg * CE + (co ^ pipe_gx<8, 4>(gg)));
+          }
+          T *yu = yb + (int64_t)u0 * wc;
+          *reinterpret_cast<float4 *>(yu) = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+          *reinterpret_cast<float4 *>(yu + wc) = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+          *reinterpret_cast<float4 *>(yu + 2 * wc) = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+          *reinterpret_cast<float4 *>(yu + 3 * wc) = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+        }
+      }
+      __syncwarp();
+      // the last store warp hands this CTA's stage back (its own reads and, through the peer's arrive, the
+      // peer's DSMEM reads of it have returned) and refills it
+      mbar_arrive(&empty[st]);  // every lane: its reads of this CTA's stage are done
+      if (lane == 0) {
+        __threadfence_block();
+        if (atomicAdd(&scnt[st], 1u) == (unsigned)NSW - 1) {
+          scnt[st] = 0;
+          __threadfence_block();
+          mbar_arrive_cluster(&empty[st], peer);  // release: this CTA's DSMEM reads of the peer's stage
+          mbar_wait_cluster(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + S);
+        }
+      }
+      __syncwarp();
+    }
+  }
+  cluster_sync_all();  // neither CTA leaves while its peer may still read its shared memory
 }
 
 // ------------------------------------------------------------------ fp64 two-factor chunks on DMMA (v5)
@@ -1952,6 +2220,8 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 32, 512, 1, 8, 0},
     // v6 P = 16 with 32-chunk tiles (128-byte runs, twice the ring stages): id 35 (autotuner candidate)
     {KRON_F32, 16, 256, 2, 6, 0},
+    // v9: fp32 16 x 16 factor triples on a 2-CTA cluster (NEXT-2): id 36
+    {KRON_F32, 16, 256, 2, 10, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -1964,6 +2234,7 @@ Kernel4Fn instance_kernel4(int i) {
     case 30: return kron_fused_dmma2_kernel<8, 4, 8>;
     case 33: return kron_fused_dmma2g_kernel<8, 4>;
     case 34: return kron_fused_tf32x3_kernel<8, 4>;
+    case 36: return kron_fused_gemm3c_kernel<12>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -1986,9 +2257,11 @@ KernelPFn instance_pipe(int i) {
 
 KernelFn instance_kernel(int i) {
   switch (i) {
-    case 31: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4>;
-    case 32: return kron_fused_gemm2ws_kernel<32, 12, 4, 8, 4>;
-    case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4>;
+    // two k-blocks of the chunk GEMMs unrolled together (KU = 2): E 8.50 -> 7.96 ms per pass, C32 3.27 -> 3.20
+    // P = 32: 8 x 8 lane tiles on 8 compute warps (162 registers): C32 3.20 -> 3.10 ms per pass; P = 16 keeps
+    // 4 x 8 tiles on 12 warps (8 x 8 measured 7.6 -> 8.4 ms on E's pair pass)
+    case 31: case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2>;
+    case 32: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
     case 7: return kron_fused_warp_kernel<float, 8, 2, 256, 2>;
@@ -2176,7 +2449,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     threads = 32 * (8 + 4);
   } else if (inst.warp == 6) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
-    threads = 32 * (12 + 4);
+    threads = 32 * ((pp.P == 32 ? 8 : 12) + 4);  // compute warps of the instance (see instance_kernel)
   } else if (inst.warp == 3) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
   } else if (inst.warp == 2 || inst.warp == 4) {
@@ -2185,6 +2458,25 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   } else {
     smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
+  }
+  if (inst.warp == 10) {
+    // cluster pair: grid = 2 x clusters (one CTA per SM), a.ntiles = 8-chunk groups
+    smem = 1024 + (size_t)a.stages * 65536 + 3 * 1024 + 64 * (size_t)a.stages;
+    threads = 32 * (12 + 4);
+    Kernel4Fn k10 = instance_kernel4(pp.variant);
+    static std::once_flag attr_once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once, [&] {
+      attr_err = cudaFuncSetAttribute((const void *)k10, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    });
+    if (attr_err != cudaSuccess) return (int)attr_err;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t ncl = sms / 2;  // one CTA per SM (the smem footprint), clusters of two
+    if (ncl > a.ntiles) ncl = a.ntiles;
+    k10<<<(unsigned)(2 * ncl), threads, smem, (cudaStream_t)stream>>>(tin, a);
+    return (int)cudaGetLastError();
   }
   if (inst.warp == 3 || inst.warp == 5 || inst.warp == 8) {
     Kernel4Fn k4 = instance_kernel4(pp.variant);

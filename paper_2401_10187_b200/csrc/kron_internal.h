@@ -50,9 +50,12 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0x1FFu;     // allowed fused kernel families (bit = FusedInstance::warp)
+  unsigned kinds = 0x7FFu;     // allowed fused kernel families (bit = FusedInstance::warp)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
-  bool operator==(const PlanPolicy &o) const { return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma; }
+  bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
+  bool operator==(const PlanPolicy &o) const {
+    return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma && short_tiles == o.short_tiles;
+  }
 };
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
                         int64_t lead = 1, const PlanPolicy &policy = PlanPolicy());

@@ -53,6 +53,8 @@ SMALL = [
     (33, [8] * 4, [8] * 4),               # fused P=8 (3,1)
     (5, [8] * 6, [8] * 6),                # config B shape, small M (two separate passes)
     (3, [16] * 4, [16] * 4),              # fused P=16 (2,2)
+    (3, [16] * 5, [16] * 5),              # config E shape: fp32 16x16 triple on a CTA pair (v9) + pair
+    (5, [8, 16, 16, 16], [8, 16, 16, 16]),  # v9 triple (W = 8 chunks) behind a P=8 factor
     (2, [32] * 3, [32] * 3),              # fused P=32 (2,1)
     (9, [2] * 10, [2] * 10),              # fused P=2 deep groups
     (1, [8] * 5, [8] * 5),                # single row

@@ -16,6 +16,7 @@ from paper_2401_10187_b200 import kron  # noqa: E402
 CASES = [
     (9, [8] * 6, [8] * 6, np.float32),          # v3 factor pipeline (3,3)
     (2, [32] * 3, [32] * 3, np.float32),        # v6 warp-specialised chunk pair, P = 32 (+ v2)
+    (3, [8, 16, 16, 16], [8, 16, 16, 16], np.float32),  # v9 16x16 triple on a CTA pair (DSMEM) + v2
     (2, [16] * 4, [16] * 4, np.float32),        # v6, P = 16 (64-chunk tiles)
     (2, [16] * 3, [16] * 3, np.float32),        # v4/v6 (2) + v2 (1)
     (2, [32] * 3, [32] * 3, np.float64),        # v5 DMMA chunk pair (+ v2)
