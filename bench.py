@@ -143,6 +143,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def max_over_ranks(v, dev):
+    """MAX of a per-rank float over the default process group (device tensor for NCCL, host for gloo)."""
+    import torch
+    import torch.distributed as dist
+    on = dev if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([v], dtype=torch.float64, device=on)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -188,7 +198,7 @@ def run_reference(args, cfg_name):
     dt = np.float32 if dtn == "float32" else np.float64
     seed = synth.SEED_BASE + cfg
     K = int(np.prod(P))
-    cores = len(os.sched_getaffinity(0))
+    cores = oracle.threads(len(os.sched_getaffinity(0)))  # all host cores (torchrun exports OMP_NUM_THREADS=1)
     per_row = flops_of(1, P, Q)
     # rows per step: ~0.15 s of oracle work at ~1 GFLOP/s/core
     rows = int(max(1, min(M, 0.15 * cores * 1e9 / per_row)))
@@ -335,9 +345,7 @@ def run_dist(args, ws, rank, local, dev, barrier):
     barrier()
     ms = t0.elapsed_time(t1)
     if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     rounds, ledger = kron.dist_plan(M, P, Q, ctx.GM, ctx.GK)
     fl_step = flops_of(M, P, Q)
     value = fl_step * args.steps / (ms / 1e3) / 1e9
@@ -407,11 +415,20 @@ def main():
     ws, rank, local = dist_env()
     if ws != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+    # KRON_BENCH_SHARE_GPU=1 (plumbing test only): every rank on cuda:0 with a gloo process group, so the
+    # N > 1 code paths (barriers, max-over-ranks, P2P heaps over CUDA IPC) run on a one-GPU box; NCCL
+    # cannot place two ranks on one device.  Numbers from such a run are not bench values.
+    share = os.environ.get("KRON_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     def barrier():
         if ws > 1:
@@ -473,9 +490,7 @@ def main():
     torch.cuda.synchronize()
     ms = t_start.elapsed_time(t_end)
     if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     fl_step = flops_of(M, P, Q)
     value = ws * fl_step * args.steps / (ms / 1e3) / 1e9  # whole-job GFLOP/s
 
@@ -544,9 +559,7 @@ def main():
         torch.cuda.synchronize()
         ems = e0.elapsed_time(e1)
         if ws > 1:
-            t = torch.tensor([ems], dtype=torch.float64, device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            ems = float(t.item())
+            ems = max_over_ranks(ems, dev)
         h2d = M * K * es + sum(f.numel() * es for f in Fh)
         e2e = {"value": round(ws * fl_step * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(M * L * es), "steps": args.e2e_steps,
@@ -555,8 +568,10 @@ def main():
 
     cpu = None
     if rank == 0 and not args.no_cpu:
+        import oracle
+        cores = oracle.threads(len(os.sched_getaffinity(0)))  # all host cores (torchrun sets OMP_NUM_THREADS=1)
         rate, rows, t, reps = cpu_oracle_rate(M, P, Q, seed, dt)
-        cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+        cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
                "sample": f"rows 0..{rows - 1} of config {args.config} (M={M}) x {reps} passes, {t:.1f} s; plain C "
                          f"fp64 Algorithm 1 (oracle/), OpenMP over rows"}
 

@@ -56,6 +56,8 @@ def lib():
         _lib.oracle_fused_store_col.restype = ctypes.c_int64
         _lib.oracle_fused_store_col.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int,
                                                 ctypes.c_int64, ctypes.c_int64]
+        _lib.oracle_threads.restype = ctypes.c_int
+        _lib.oracle_threads.argtypes = [ctypes.c_int]
         _lib.oracle_shift_pos.restype = ctypes.c_int64
         _lib.oracle_shift_pos.argtypes = [ctypes.c_int64, ctypes.c_int, ctypes.c_int]
         _lib.oracle_grid.argtypes = [ctypes.c_int, _I, _I]
@@ -160,3 +162,9 @@ def grid(G: int):
     if rc != 0:
         return None
     return gm.value, gk.value
+
+
+def threads(n: int = 0) -> int:
+    """OpenMP threads of the row-parallel loops: n > 0 sets the count (torchrun exports
+    OMP_NUM_THREADS=1 to every rank); returns the count in effect.  Results do not depend on it."""
+    return int(lib().oracle_threads(int(n)))

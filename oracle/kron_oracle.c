@@ -24,6 +24,7 @@
  * Return codes: 0 ok, 1 invalid argument, 2 too large / shape error, 3 out of memory.
  */
 #include <stdint.h>
+#include <omp.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -359,4 +360,11 @@ done:
   free(col);
   free(tcol);
   return ret;
+}
+
+/* OpenMP thread count for the row-parallel loops (infrastructure only: rows are independent, so the
+ * result does not depend on it).  n > 0 sets it; returns the count the next parallel region uses. */
+int oracle_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
 }
