@@ -103,7 +103,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     stages = 4;  // two co-resident CTAs (one per pass) per SM
   } else if (inst.warp == 2) {
     nout = 2;
-    stages = (int)((200 * 1024 - 2 * stage) / stage);  // deep ring: one CTA per SM
+    // deep ring: one CTA per SM, as many stages as the 227 KB allow next to the two output tiles
+    // (config B: 5 x 32 KB stages, 0.743 -> 0.726 ms vs 4)
+    stages = (int)((227 * 1024 - 1024 - 2 * stage - 512) / stage);
     if (stages > 8) stages = 8;
     if (stages < k + 1) return false;
   } else if (inst.warp == 1) {
