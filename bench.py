@@ -379,7 +379,7 @@ def run_dist(args, ws, rank, local, dev, barrier):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=100)  # the paper: "average of 100 runs after 10 warm-ups"
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
