@@ -173,7 +173,7 @@ kron_status_t cuda_fail(int err, const char *what) {
 }
 
 kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
-                       void *const *events = nullptr) {
+                       void *const *events = nullptr, const PushArgs *push = nullptr) {
   const size_t es = es_of(plan.dtype);
   int ip = 0;
   void *bufs[4] = {const_cast<void *>(X), Y, ws,
@@ -190,7 +190,8 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
       const int nfac = pp.pair ? 2 * pp.nf : pp.nf;
       for (int i = 0; i < nfac; ++i) grp[i] = F[pp.first - 1 - i];
       void *aux = ws ? static_cast<char *>(ws) + (size_t)plan.nws * plan.ws_elems * es : nullptr;
-      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, aux, stream);
+      const bool lastp = &pp == &plan.passes.back();
+      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, aux, stream, lastp ? push : nullptr);
     } else if (pp.kind == KIND_GEMM) {
       err = launch_gemm(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
     } else {
@@ -228,8 +229,15 @@ void keep_pool_cached() {
 
 size_t plan_ws_bytes(const Plan &plan) { return ws_bytes_of(plan); }
 
-kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream) {
-  return run_plan(plan, X, F, Y, ws, stream);
+kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
+                       const PushArgs *push) {
+  return run_plan(plan, X, F, Y, ws, stream, nullptr, push);
+}
+
+bool plan_push_ok(const Plan &plan) {
+  if (plan.passes.empty()) return false;
+  const PassPlan &pp = plan.passes.back();
+  return pp.kind == KIND_FUSED && !pp.pair && fused_instance(pp.variant).warp == 10;
 }
 
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {

@@ -646,6 +646,7 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     return KRON_ERR_NO_MEMORY;
   }
 
+  int p2p_in_half = -1;  // P2P: heap half holding this round's input block (after a push round), else -1
   for (size_t j = 0; j < rounds.size() && st == KRON_OK; ++j) {
     const RoundPlan &R = rp[j];
     const int k = rounds[j];
@@ -654,25 +655,51 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     const int64_t B = R.wl_out / GK;       // values per row sent to each peer
     const size_t blk = (size_t)Ml * B;     // values per peer
     if (p2p) {
+      PeerPtrs heaps{};
+      for (int g = 0; g < GK; ++g) heaps.p[g] = ctx->peer_heap[g];
+      auto barrier = [&]() {
+        const unsigned long long ep = ++ctx->epoch;
+        p2p_barrier_kernel<<<1, 64, 0, s>>>(heaps, reinterpret_cast<unsigned long long *>(ctx->heap), GK, ctx->gK,
+                                            ep, reinterpret_cast<unsigned *>(ctx->heap + kP2PTimeoutOff),
+                                            (long long)20 * 1000 * 1000 * 1000);
+        return cudaGetLastError() == cudaSuccess;
+      };
+      // this round writes the heap half its input does not occupy
+      const int out_half = p2p_in_half >= 0 ? 1 - p2p_in_half : (int)ctx->parity;
+      const size_t off = kP2PHeader + (size_t)out_half * half;
+      const void *in = j == 0 ? Xv[0] : (p2p_in_half >= 0 ? (const void *)(ctx->heap + kP2PHeader +
+                                                                           (size_t)p2p_in_half * half)
+                                                          : (const void *)bufs[0].cur);
+      ctx->parity = 1u - (unsigned)out_half;
+      if (!last && GK <= kMaxPush && plan_push_ok(R.plan) && !getenv("KRON_P2P_NO_PUSH")) {
+        // FUSED exchange: the round's last pass stores every value straight into its StoreGPUTile position
+        // in the destination rank's heap half (peer memory over NVLink), so the transfer overlaps the
+        // arithmetic tile by tile.  Barrier before (every rank finished reading that half and pulling from
+        // the previous round) and after (every value addressed to this rank has landed).
+        if (!barrier()) { st = KRON_ERR_CUDA; break; }
+        PushArgs pa;
+        for (int g = 0; g < GK; ++g) pa.dst[g] = ctx->peer_heap[g] + off;
+        pa.B = B;
+        pa.rho = R.rho;
+        pa.wd = R.wl_out;
+        pa.GK = GK;
+        pa.me = ctx->gK;
+        pa.on = 1;
+        st = plan_run(R.plan, in, Fj, ctx->heap + off, bufs[0].ws, stream, &pa);
+        if (st != KRON_OK) break;
+        if (!barrier()) { st = KRON_ERR_CUDA; break; }
+        p2p_in_half = out_half;  // the next round reads its block from this rank's own heap half
+        continue;
+      }
       // lines 670-674 into this rank's heap half, barrier, then lines 676-690 + 685 as one pull kernel
-      const size_t off = kP2PHeader + (size_t)ctx->parity * half;
-      const void *in = j == 0 ? Xv[0] : bufs[0].cur;
       st = plan_run(R.plan, in, Fj, ctx->heap + off, bufs[0].ws, stream);
       if (st != KRON_OK) break;
-      PeerPtrs heaps{}, outs{};
-      for (int g = 0; g < GK; ++g) {
-        heaps.p[g] = ctx->peer_heap[g];
-        outs.p[g] = ctx->peer_heap[g] + off;
-      }
-      const unsigned long long ep = ++ctx->epoch;
-      p2p_barrier_kernel<<<1, 64, 0, s>>>(heaps, reinterpret_cast<unsigned long long *>(ctx->heap), GK, ctx->gK, ep,
-                                          reinterpret_cast<unsigned *>(ctx->heap + kP2PTimeoutOff),
-                                          (long long)20 * 1000 * 1000 * 1000);
-      if (cudaGetLastError() != cudaSuccess) st = KRON_ERR_CUDA;
+      PeerPtrs outs{};
+      for (int g = 0; g < GK; ++g) outs.p[g] = ctx->peer_heap[g] + off;
+      if (!barrier()) { st = KRON_ERR_CUDA; break; }
       void *dst = last ? Yv[0] : bufs[0].cur;
-      if (st == KRON_OK && launch_p2p_pull((int)dtype, outs, dst, Ml, R.wl_out, R.rho, GK, ctx->gK, s) != 0)
-        st = KRON_ERR_CUDA;
-      ctx->parity ^= 1u;
+      if (launch_p2p_pull((int)dtype, outs, dst, Ml, R.wl_out, R.rho, GK, ctx->gK, s) != 0) st = KRON_ERR_CUDA;
+      p2p_in_half = -1;
       continue;
     }
     // lines 670-674: local sliced multiplies; then pack the destination-major send buffer

@@ -63,6 +63,7 @@ struct FusedArgs {
   uint32_t tile_bytes;
   uint32_t stage_bytes;
   int stages;
+  PushArgs push;  // v9: distributed P2P push of the pass's output (push.on)
 };
 
 namespace {
@@ -1615,11 +1616,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
             const uint32_t gg = (uint32_t)(t * 16) + q3;
             v[t] = ld_dsmem_f32x4(sb + gg * CE + (co ^ pipe_gx<8, 4>(gg)));
           }
-          T *yu = yb + (int64_t)u0 * wc;
-          *reinterpret_cast<float4 *>(yu) = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
-          *reinterpret_cast<float4 *>(yu + wc) = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
-          *reinterpret_cast<float4 *>(yu + 2 * wc) = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
-          *reinterpret_cast<float4 *>(yu + 3 * wc) = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+          const float4 o4[4] = {make_float4(v[0].x, v[1].x, v[2].x, v[3].x), make_float4(v[0].y, v[1].y, v[2].y, v[3].y),
+                                make_float4(v[0].z, v[1].z, v[2].z, v[3].z), make_float4(v[0].w, v[1].w, v[2].w, v[3].w)};
+          if (!a.push.on) {
+            T *yu = yb + (int64_t)u0 * wc;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) *reinterpret_cast<float4 *>(yu + j * wc) = o4[j];
+          } else {
+            // distributed round (NEXT-1, fused): the 16-byte run goes straight to its StoreGPUTile position
+            // in the destination rank's next-round block over NVLink (runs of rho never split: rho % 4 == 0)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int64_t col = (int64_t)(u0 + j) * wc + (int64_t)gj * 8 + h * 4;
+              const int64_t d = col / a.push.B, e = col - d * a.push.B;
+              const int64_t run = e / a.push.rho;
+              const int64_t tcol = (run * a.push.GK + a.push.me) * a.push.rho + (e - run * a.push.rho);
+              *reinterpret_cast<float4 *>(reinterpret_cast<T *>(a.push.dst[d]) + (int64_t)rb * a.push.wd + tcol) = o4[j];
+            }
+          }
         }
       }
       __syncwarp();
@@ -2372,7 +2386,7 @@ int fused_find(int dtype, int P, int warp) {
 }
 
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *aux, void *stream) {
+                 void *aux, void *stream, const PushArgs *push) {
   const FusedInstance &inst = kInstances[pp.variant];
   const int es = dtype == KRON_F32 ? 4 : 8;
   const int line = 128 / es;
@@ -2474,6 +2488,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   } else {
     smem = 1024 + (size_t)(a.stages + (inst.warp ? pp.nout : 0)) * a.stage_bytes +
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
+  }
+  if (push && push->on) {
+    if (inst.warp != 10 || push->GK > kMaxPush) return (int)cudaErrorInvalidValue;
+    a.push = *push;
   }
   if (inst.warp == 10) {
     // cluster pair: grid = 2 x clusters (one CTA per SM), a.ntiles = 8-chunk groups

@@ -60,9 +60,21 @@ struct PlanPolicy {
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
                         int64_t lead = 1, const PlanPolicy &policy = PlanPolicy());
 size_t plan_ws_bytes(const Plan &plan);
+// Distributed P2P push (NEXT-1): the LAST pass of a plan writes every output value straight to its
+// StoreGPUTile position in the destination rank's buffer (peer memory).  Output column c of the local
+// block goes to rank d = c / B at column ((e / rho) * GK + me) * rho + e % rho, e = c % B, of a row of
+// width wd.  Only kernels whose store path implements it (plan_push_ok) are driven this way.
+constexpr int kMaxPush = 8;
+struct PushArgs {
+  void *dst[kMaxPush] = {};
+  int64_t B = 0, rho = 0, wd = 0;
+  int GK = 0, me = 0, on = 0;
+};
+bool plan_push_ok(const Plan &plan);
 void keep_pool_cached();  // default mem pool keeps freed blocks (stream-ordered workspaces)
 // Enqueue every pass of `plan` (F indexed like the plan's P/Q arrays); ws >= plan_ws_bytes bytes.
-kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream);
+kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
+                       const PushArgs *push = nullptr);
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype);
 
 // ---- fused small-P kernel family (fused.cu)
@@ -83,7 +95,7 @@ int fused_find(int dtype, int P, int warp);  // instance id or -1
 int launch_generic(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F,
                    void *stream);
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *aux, void *stream);
+                 void *aux, void *stream, const PushArgs *push = nullptr);
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 

@@ -25,7 +25,9 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, GM, GK, M, P, Q, q):
+def _worker(rank, world, port, GM, GK, M, P, Q, q, push=True):
+    if not push:
+        os.environ["KRON_P2P_NO_PUSH"] = "1"  # every round through the pull kernel
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -67,7 +69,8 @@ def _worker(rank, world, port, GM, GK, M, P, Q, q):
 
 GRIDS = [
     # (GM, GK, M, P, Q)
-    (1, 2, 4, [16] * 5, [16] * 5),    # config E shapes, K split only (2 rounds)
+    (1, 2, 4, [16] * 5, [16] * 5),    # config E shapes, K split only (2 rounds; round 1 pushes from v9)
+    (2, 2, 4, [16] * 5, [16] * 5),    # paper rule for 4 GPUs on E shapes (push + pull)
     (2, 2, 4, [8] * 4, [8] * 4),      # paper rule for 4 GPUs
     (1, 4, 2, [4] * 4, [4] * 4),      # Fig 8 {1,4}: K = 256, Local = 2
     (1, 2, 2, [8, 4, 4], [4, 8, 4]),  # mixed, non-square (scalar pull path)
@@ -75,14 +78,18 @@ GRIDS = [
 
 
 @pytest.mark.timeout(600)
+@pytest.mark.parametrize("push", [True, False])
 @pytest.mark.parametrize("GM,GK,M,P,Q", GRIDS)
-def test_dist_p2p(GM, GK, M, P, Q):
+def test_dist_p2p(GM, GK, M, P, Q, push):
+    """push=True: rounds whose last pass is the v9 cluster kernel store straight into the peers' heaps
+    (the fused exchange); every other round, and every round with push=False, goes through the pull
+    kernel."""
     import torch.multiprocessing as mp
     world = GM * GK
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, GM, GK, M, P, Q, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, GM, GK, M, P, Q, q, push)) for r in range(world)]
     for p in procs:
         p.start()
     res = sorted(q.get(timeout=500) for _ in range(world))
