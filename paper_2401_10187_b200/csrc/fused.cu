@@ -1378,7 +1378,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
 // store warp, release.cluster: both CTAs' reads of this stage are done).  Warps: 12 compute, 3 store,
 // 1 signal.
 // compute-sanitizer racecheck / synccheck / memcheck clean (tools/sanitize.py).
-template <int NCW>
+template <int NCW, bool PUSH = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
     kron_fused_gemm3c_kernel(const __grid_constant__ CUtensorMap tm_in, const FusedArgs a) {
   using T = float;
@@ -1618,7 +1618,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
           }
           const float4 o4[4] = {make_float4(v[0].x, v[1].x, v[2].x, v[3].x), make_float4(v[0].y, v[1].y, v[2].y, v[3].y),
                                 make_float4(v[0].z, v[1].z, v[2].z, v[3].z), make_float4(v[0].w, v[1].w, v[2].w, v[3].w)};
-          if (!a.push.on) {
+          if constexpr (!PUSH) {
             T *yu = yb + (int64_t)u0 * wc;
 #pragma unroll
             for (int j = 0; j < 4; ++j) *reinterpret_cast<float4 *>(yu + j * wc) = o4[j];
@@ -2497,13 +2497,14 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     // cluster pair: grid = 2 x clusters (one CTA per SM), a.ntiles = 8-chunk groups
     smem = 1024 + (size_t)a.stages * 65536 + 3 * 1024 + 80 * (size_t)a.stages;
     threads = 32 * (12 + 4);
-    Kernel4Fn k10 = instance_kernel4(pp.variant);
-    static std::once_flag attr_once;
-    static cudaError_t attr_err = cudaSuccess;
-    std::call_once(attr_once, [&] {
-      attr_err = cudaFuncSetAttribute((const void *)k10, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    Kernel4Fn k10 = a.push.on ? kron_fused_gemm3c_kernel<12, true> : instance_kernel4(pp.variant);
+    static std::once_flag attr_once[2];
+    static cudaError_t attr_err[2] = {cudaSuccess, cudaSuccess};
+    const int ki = a.push.on ? 1 : 0;
+    std::call_once(attr_once[ki], [&] {
+      attr_err[ki] = cudaFuncSetAttribute((const void *)k10, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     });
-    if (attr_err != cudaSuccess) return (int)attr_err;
+    if (attr_err[ki] != cudaSuccess) return (int)attr_err[ki];
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
