@@ -92,9 +92,21 @@ def test_dist_p2p(GM, GK, M, P, Q, push):
     procs = [ctx.Process(target=_worker, args=(r, world, port, GM, GK, M, P, Q, q, push)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=500) for _ in range(world))
+    import queue
+    import time
+    res, t0 = [], time.time()
+    while len(res) < world and time.time() - t0 < 300:
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            if not any(p.is_alive() for p in procs):  # a rank died without reporting: fail fast
+                break
     for p in procs:
         p.join(timeout=60)
+        if p.is_alive():
+            p.kill()
+    assert len(res) == world, f"only {len(res)} of {world} ranks reported (exit codes {[p.exitcode for p in procs]})"
+    res.sort()
     for rank, ok, timeouts in res:
         assert all(v is True for v in ok), f"rank {rank}: {ok}"
         assert timeouts == 0, f"rank {rank}: {timeouts} barrier timeouts"
