@@ -172,8 +172,9 @@ kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32
  *        process (`rank` = this process's rank, nccl_unique_id ignored).  Before the first call the
  *        ranks reserve a symmetric heap (kron_dist_p2p_reserve), exchange its 64-byte CUDA IPC
  *        handles (e.g. all_gather over a torch ProcessGroup) and map the row-group peers' heaps
- *        (kron_dist_p2p_connect).  A round whose last local pass is the fp32 16x16 cluster kernel
- *        (and that is not the last round) FUSES the exchange into that pass: its store warps write
+ *        (kron_dist_p2p_connect).  A round whose last local pass is the fp32 16x16 cluster kernel or
+ *        an fp32 16x16 / 32x32 chunk-pair kernel (and that is not the last round) FUSES the exchange
+ *        into that pass: its store warps write
  *        every value straight into its StoreGPUTile position in the destination rank's heap (peer
  *        stores over NVLink / NVSwitch), between two device-side flag barriers.  Every other round
  *        writes its local output into this rank's heap, meets the row group at a flag barrier, and

@@ -237,7 +237,9 @@ kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, vo
 bool plan_push_ok(const Plan &plan) {
   if (plan.passes.empty()) return false;
   const PassPlan &pp = plan.passes.back();
-  return pp.kind == KIND_FUSED && !pp.pair && fused_instance(pp.variant).warp == 10;
+  if (pp.kind != KIND_FUSED || pp.pair) return false;
+  const FusedInstance &fi = fused_instance(pp.variant);
+  return fi.warp == 10 || (fi.warp == 6 && fi.dtype == KRON_F32 && (fi.P == 16 || fi.P == 32));
 }
 
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {

@@ -1129,7 +1129,16 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
 // full = landed, cdone = computed, empty = streamed out -> refill).  Output runs are R*4 bytes; the
 // measured write rate of such runs (tools/microbench_scatter.cu: 2.9 TB/s at 32 B, 4.5 TB/s at 128 B,
 // profiles/r01_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
-template <int P, int NCW, int RM, int RN, int VA, int KU = 1>
+// PUSH: distributed P2P round whose exchange is fused into this pass (NEXT-1): every output value is
+// stored at its StoreGPUTile position in the destination rank's heap instead of into Y (push_dst).
+template <typename T>
+__device__ __forceinline__ T *push_dst(const FusedArgs &a, int rb, int64_t col) {
+  const int64_t d = col / a.push.B, e = col - d * a.push.B, run = e / a.push.rho;
+  const int64_t tcol = (run * a.push.GK + a.push.me) * a.push.rho + (e - run * a.push.rho);
+  return reinterpret_cast<T *>(a.push.dst[d]) + (int64_t)rb * a.push.wd + tcol;
+}
+
+template <int P, int NCW, int RM, int RN, int VA, int KU = 1, bool PUSH = false>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                               const __grid_constant__ CUtensorMap tm_out,
                                                                               const FusedArgs a) {
@@ -1318,10 +1327,18 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
             for (int h = 0; h < a.R / 32; ++h) {
               const float4 v = *reinterpret_cast<const float4 *>(buf + (uint32_t)(h * 32 + lane) * CE +
                                                                  (swz128(u * ES) ^ gxl));
-              p[h * 32] = v.x;
-              p[h * 32 + wc] = v.y;
-              p[h * 32 + 2 * wc] = v.z;
-              p[h * 32 + 3 * wc] = v.w;
+              if constexpr (PUSH) {
+                const int64_t c0 = (int64_t)u * wc + (int64_t)cbk * a.R + h * 32 + lane;
+                *push_dst<T>(a, rb, c0) = v.x;
+                *push_dst<T>(a, rb, c0 + wc) = v.y;
+                *push_dst<T>(a, rb, c0 + 2 * wc) = v.z;
+                *push_dst<T>(a, rb, c0 + 3 * wc) = v.w;
+              } else {
+                p[h * 32] = v.x;
+                p[h * 32 + wc] = v.y;
+                p[h * 32 + 2 * wc] = v.z;
+                p[h * 32 + 3 * wc] = v.w;
+              }
             }
           }
         } else
@@ -1337,11 +1354,19 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
             for (int u16 = sw; u16 < C / 16; u16 += NSW) {
               const uint32_t u = (uint32_t)(u16 * 16 + uq * 4);
               const float4 v = *reinterpret_cast<const float4 *>(ch + (swz128(u * ES) ^ gx));
-              T *p = yg + (int64_t)u * wc;
-              p[0] = v.x;
-              p[wc] = v.y;
-              p[2 * wc] = v.z;
-              p[3 * wc] = v.w;
+              if constexpr (PUSH) {
+                const int64_t c0 = (int64_t)u * wc + gcol;
+                *push_dst<T>(a, rb, c0) = v.x;
+                *push_dst<T>(a, rb, c0 + wc) = v.y;
+                *push_dst<T>(a, rb, c0 + 2 * wc) = v.z;
+                *push_dst<T>(a, rb, c0 + 3 * wc) = v.w;
+              } else {
+                T *p = yg + (int64_t)u * wc;
+                p[0] = v.x;
+                p[wc] = v.y;
+                p[2 * wc] = v.z;
+                p[3 * wc] = v.w;
+              }
             }
           }
         }
@@ -2490,7 +2515,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
   }
   if (push && push->on) {
-    if (inst.warp != 10 || push->GK > kMaxPush) return (int)cudaErrorInvalidValue;
+    if ((inst.warp != 10 && inst.warp != 6) || push->GK > kMaxPush) return (int)cudaErrorInvalidValue;
     a.push = *push;
   }
   if (inst.warp == 10) {
@@ -2549,6 +2574,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     return (int)cudaLaunchKernelEx(&cfg, kp, tin, tout, a, tin2, tout2);
   }
   KernelFn k = instance_kernel(pp.variant);
+  if (a.push.on) {  // v6 with the fused exchange (same tiling, push epilogue)
+    k = pp.P == 32 ? kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, true> : kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true>;
+  }
   const int slots = kernel_slots((const void *)k, threads, smem);
   if (slots < 1) return (int)cudaErrorInvalidConfiguration;
   int64_t grid = slots;

@@ -71,6 +71,8 @@ GRIDS = [
     # (GM, GK, M, P, Q)
     (1, 2, 4, [16] * 5, [16] * 5),    # config E shapes, K split only (2 rounds; round 1 pushes from v9)
     (2, 2, 4, [16] * 5, [16] * 5),    # paper rule for 4 GPUs on E shapes (push + pull)
+    (1, 2, 2, [16] * 4, [16] * 4),    # round 1 = P=16 chunk pairs (v6, 256-byte-run store path) pushing
+    (1, 2, 2, [32] * 4, [32] * 4),    # round 1 = P=32 chunk pairs (v6, chunk-octet store path) pushing
     (2, 2, 4, [8] * 4, [8] * 4),      # paper rule for 4 GPUs
     (1, 4, 2, [4] * 4, [4] * 4),      # Fig 8 {1,4}: K = 256, Local = 2
     (1, 2, 2, [8, 4, 4], [4, 8, 4]),  # mixed, non-square (scalar pull path)
@@ -81,9 +83,9 @@ GRIDS = [
 @pytest.mark.parametrize("push", [True, False])
 @pytest.mark.parametrize("GM,GK,M,P,Q", GRIDS)
 def test_dist_p2p(GM, GK, M, P, Q, push):
-    """push=True: rounds whose last pass is the v9 cluster kernel store straight into the peers' heaps
-    (the fused exchange); every other round, and every round with push=False, goes through the pull
-    kernel."""
+    """push=True: non-final rounds whose last pass is the v9 cluster kernel or a v6 fp32 chunk-pair
+    kernel store straight into the peers' heaps (the fused exchange); every other round, and every round
+    with push=False, goes through the pull kernel."""
     import torch.multiprocessing as mp
     world = GM * GK
     ctx = mp.get_context("spawn")
