@@ -1403,7 +1403,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
 // store warp, release.cluster: both CTAs' reads of this stage are done).  Warps: 12 compute, 3 store,
 // 1 signal.
 // compute-sanitizer racecheck / synccheck / memcheck clean (tools/sanitize.py).
-template <int NCW, bool PUSH = false>
+// P2W: columns per lane in phase 2 (16: one unit = a 16 x 128 block, fewer shared loads per FMA than
+// 8: E's v9 pass 11.73 -> 11.62 ms)
+template <int NCW, bool PUSH = false, int P2W = 16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
     kron_fused_gemm3c_kernel(const __grid_constant__ CUtensorMap tm_in, const FusedArgs a) {
   using T = float;
@@ -1411,7 +1413,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   constexpr uint32_t CE = C1 * ES;                // subchunk bytes (1 KB)
   constexpr int NSW = 4, L1 = (P / RM) * (P / RN), CPG = 32 / L1;
   constexpr int SUB = 64;                         // subchunks per CTA tile (4 chunks of 4096)
-  constexpr int U1 = SUB / CPG, U2 = 16, UPT = U1 + U2;
+  constexpr int U1 = SUB / CPG, U2 = 2 * 64 / P2W, UPT = U1 + U2;  // phase-2 units: 8 * P2W columns each
   constexpr uint32_t TB = SUB * CE;               // 64 KB per CTA tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1468,11 +1470,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
 
   if (warp < NCW) {
     // one warp-level P x P x P product with 128B-swizzled A rows arow[] (k in blocks of 8)
-    auto gemm = [&](const unsigned char *A, const uint32_t (&arow)[RM], auto loadB, T (&acc)[RM][RN]) {
+    auto gemm = [&](const unsigned char *A, const uint32_t (&arow)[RM], auto loadB, auto &acc) {
+      constexpr int NN = sizeof(acc[0]) / sizeof(T);
 #pragma unroll
       for (int i = 0; i < RM; ++i)
 #pragma unroll
-        for (int j = 0; j < RN; ++j) acc[i][j] = 0.f;
+        for (int j = 0; j < NN; ++j) acc[i][j] = 0.f;
 #pragma unroll 2
       for (int k0 = 0; k0 < P; k0 += 8) {
         uint32_t ab[RM];
@@ -1488,13 +1491,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
           }
 #pragma unroll
           for (int e = 0; e < VA; ++e) {
-            T f[RN];
+            T f[NN];
             loadB(k0, kk + e, f);
 #pragma unroll
             for (int i = 0; i < RM; ++i) {
               const float2 xx = make_float2(xa[i][e], xa[i][e]);
 #pragma unroll
-              for (int j = 0; j < RN; j += 2) {
+              for (int j = 0; j < NN; j += 2) {
                 const float2 r2 = __ffma2_rn(xx, make_float2(f[j], f[j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
                 acc[i][j] = r2.x;
                 acc[i][j + 1] = r2.y;
@@ -1528,7 +1531,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
       // unit order inside a tile (groups of 4 units): phase 1 of chunks 0, 1, 2, phase 2 of chunk 0, phase 1
       // of chunk 3, phase 2 of chunks 1, 2, 3 — a chunk's phase 2 starts about one wave of units after its
       // phase 1, so the p1 waits rarely block
-      constexpr unsigned kOrder = 0x76534210u;  // nibble i = (phase 2 ? 4 : 0) + chunk of group i
+      // (P2W = 16: phase-2 groups cover two chunks: p1 c0, p1 c1, p2 {c0,c1}, p1 c2, p1 c3, p2 {c2,c3})
+      constexpr unsigned kOrder = P2W == 8 ? 0x76534210u : 0x532410u;  // nibble i = (p2 ? 4 : 0) + index
       const int og = (int)((kOrder >> (4 * (wu / 4))) & 15u);
       const int w = og < 4 ? og * 4 + wu % 4 : U1 + (og - 4) * 4 + wu % 4;
       if (w < U1) {
@@ -1572,24 +1576,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
         __syncwarp();
         mbar_arrive(&p1[4 * st + (int)(gg / 16)]);
       } else {
-        const int w2 = w - U1, t = w2 / 4, cb = w2 % 4;
+        constexpr int UPC = 256 / (8 * P2W);  // phase-2 units per chunk
+        const int w2 = w - U1, t = w2 / UPC, cb = w2 % UPC;
         mbar_wait(&p1[4 * st + t], par);
-        const uint32_t cofs = swz128((uint32_t)(cb * 64 + cg * 8) * ES);
+        const uint32_t cofs = swz128((uint32_t)(cb * 8 * P2W + cg * P2W) * ES);
         unsigned char *cbase = buf + (uint32_t)(t * 16) * CE;
-        gemm(F3Ts, arow2, [&](int k0, int kk, T (&f)[RN]) {  // OUT = F3^T . S over the 16 subchunks
+        T acc2[RM][P2W];
+        gemm(F3Ts, arow2, [&](int k0, int kk, T (&f)[P2W]) {  // OUT = F3^T . S over the 16 subchunks
           // subchunk t*16 + k: its granule XOR depends on k mod 8 only (t*16 = 0 mod 8)
           const uint32_t o = (uint32_t)(k0 + kk) * CE + (cofs ^ pipe_gx<8, 4>((uint32_t)(k0 + kk)));
-          const float4 v0 = *reinterpret_cast<const float4 *>(cbase + o);
-          const float4 v1 = *reinterpret_cast<const float4 *>(cbase + (o ^ 16u));
-          f[0] = v0.x; f[1] = v0.y; f[2] = v0.z; f[3] = v0.w;
-          f[4] = v1.x; f[5] = v1.y; f[6] = v1.z; f[7] = v1.w;
-        }, acc);
+#pragma unroll
+          for (int g4 = 0; g4 < P2W / 4; ++g4) {
+            const float4 v = *reinterpret_cast<const float4 *>(cbase + (o ^ (16u * g4)));
+            f[4 * g4] = v.x; f[4 * g4 + 1] = v.y; f[4 * g4 + 2] = v.z; f[4 * g4 + 3] = v.w;
+          }
+        }, acc2);
         __syncwarp();  // every lane's reads of the column block are done before it is overwritten
 #pragma unroll
         for (int i = 0; i < RM; ++i) {
           const uint32_t o = (uint32_t)(sg2 + 4 * i) * CE + (cofs ^ pipe_gx<8, 4>((uint32_t)(sg2 + 4 * i)));
-          *reinterpret_cast<float4 *>(cbase + o) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-          *reinterpret_cast<float4 *>(cbase + (o ^ 16u)) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+#pragma unroll
+          for (int g4 = 0; g4 < P2W / 4; ++g4)
+            *reinterpret_cast<float4 *>(cbase + (o ^ (16u * g4))) =
+                make_float4(acc2[i][4 * g4], acc2[i][4 * g4 + 1], acc2[i][4 * g4 + 2], acc2[i][4 * g4 + 3]);
         }
         __syncwarp();
         // the last phase-2 unit of the tile publishes it to both CTAs (one cluster-scope release per tile,
