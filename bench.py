@@ -1,20 +1,28 @@
 #!/usr/bin/env python
-"""bench.py — Kron-Matmul throughput on B200 (BASELINE.json metric: "Kron-Matmul GFLOP/s and % roofline").
+"""bench.py — Kron-Matmul throughput on B200 (BASELINE.json metric: "Kron-Matmul GFLOP/s and % roofline at
+1/2/4/8 B200, fp32 and fp64").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config B] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config E] [--impl ours|reference]
 
 A step is one whole Kron-Matmul Y = X·(F^1 ⊗ … ⊗ F^N) over the configuration's full M rows (all passes
-of the plan).  Default workload: config B (BASELINE.json configs[1]: M=1024, 6 factors 8x8, fp32).
-FLOPs are the method's algorithmic count sum_f 2·M·W_f·Q_f (north_star).
+of the plan).  Default workload: config E (BASELINE.json configs[4]: M=4096, 5 factors 16x16, fp32 — the
+largest single-GPU configuration and the distributed one).  FLOPs are the method's algorithmic count
+sum_f 2·M·W_f·Q_f (north_star).
+
+N = 1: `value` times kron_matmul on config E.  The same JSON line carries device-timed sub-lines for the
+other full-size configurations (B, C32, C64, D1, D2 — BASELINE.json configs[1..3]) under "configs", each
+with its own roofline, clocks, mean / median / min step time (--no-subconfigs skips them).
+
+N > 1 (torchrun, one rank per GPU, NCCL): Algorithm 2 — kron_matmul_dist over NCCL on the paper-rule grid
+{GM,GK} (2 -> {2,1}, 4 -> {2,2}, 8 -> {4,2}) with config E's M = 4096 rows split over the
+grid -> "scaling": "strong".  A secondary row-only {G,1} measurement (no exchange) is reported
+under "row_only".  --grid GMxGK overrides the grid.
 
 Timing: W untimed warm-ups, then exactly K steps on the device between CUDA events on the launching
 stream, bracketed by barrier + synchronize, max over ranks.  Inputs (>= 1 GiB) are larger than the
-126 MB L2, so no flush is needed.  Clocks and throttle reasons are sampled with NVML during the
-timed region.  Per-pass CUDA events (kron_matmul_ws_events) give the dominant kernel's average
-launch time for the roofline object.
-
-N > 1 (torchrun, one rank per GPU): every rank runs the configuration on its own block of rows of
-a taller X (row partition: no communication) -> "scaling": "weak".
+126 MB L2, so no flush is needed.  Clocks and throttle reasons are sampled with NVML during every timed
+region.  Per-pass CUDA events (kron_matmul_ws_events) give the dominant kernel's average launch time
+for the roofline object.
 
 --impl reference times the CPU oracle (oracle/, plain C fp64 Algorithm 1) on the host cores, each
 step a bounded row sample of the same workload (this tier's reference arm).
@@ -44,7 +52,13 @@ CONFIGS = {
     "D1": (3, 320, [128] * 3, [128] * 3, "float64"),
     "D2": (4, 320, [64] * 3, [32] * 3, "float64"),
     "E": (5, 4096, [16] * 5, [16] * 5, "float32"),
+    # Fig 11 weak-scaling workloads: fp32, N = 4, M grows with the GPU count
+    # (memory per GPU constant: 16 GiB of X per GPU); M given per GPU, --dist only
+    "W64": (6, 256, [64] * 4, [64] * 4, "float32"),
+    "W128": (7, 16, [128] * 4, [128] * 4, "float32"),
 }
+WEAK = {"W64", "W128"}
+SUBCONFIGS = ["B", "C32", "C64", "D1", "D2"]
 
 # ALU peaks derived from the B200 unit counts:
 # 148 SMs x 128 FP32 lanes x 2 flop x 1.965 GHz; FP64 = half the FP32 lanes.
@@ -82,14 +96,29 @@ def measured_peaks():
 
 
 def ncu_traffic(config, kernel_prefix):
-    """dram read+write bytes per launch from the committed ncu --set full summary, if present."""
+    """dram read+write bytes per launch of the kernel from the committed `ncu --set full` capture
+    (profiles/ncu_traffic.json, written by tools/ncu_summary.py), with the capture's tag; (None, None) if the
+    kernel was not captured.  ncu replays kernels, so this cannot be measured inside the timed run."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d.get(config, {}).get(kernel_prefix)
+        v = d.get(config, {}).get(kernel_prefix)
+        return v, d.get("_source", "profiles/ncu_traffic.json")
     except Exception:
-        return None
+        return None, None
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -214,10 +243,11 @@ def run_reference(args, cfg_name):
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": ws,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(el / args.steps * 1e3, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded counter-based U[0,1))",
+        "higher_is_better": True, "scaling": "strong" if ws > 1 and cfg_name not in WEAK else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded counter-based U[0,1))",
         "config": {"workload": cfg_name, "M": M, "P": P, "Q": Q, "input_dtype": dtn, "rows_per_step": rows},
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+                         "cpu_model": cpu_model(),
                          "sample": f"rows 0..{rows - 1} of config {cfg_name} (M={M}) per step; plain C fp64 "
                                    f"Algorithm 1, OpenMP over rows"},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -303,76 +333,330 @@ def run_sweep(args):
     return 0
 
 
-def run_dist(args, ws, rank, local, dev, barrier):
-    """Strong scaling of one configuration over a {GM,GK} grid with kron_matmul_dist (NCCL)."""
-    import torch
-    import synth
-    from paper_2401_10187_b200 import kron
-    cfg, M, P, Q, dtn = CONFIGS[args.config]
+def step_stats(step_ms):
+    a = np.asarray(step_ms, dtype=np.float64)
+    return {"mean_ms": round(float(a.mean()), 5), "median_ms": round(float(np.median(a)), 5),
+            "min_ms": round(float(a.min()), 5), "max_ms": round(float(a.max()), 5)}
+
+
+def roofline_of(M, P, Q, es, alg_bytes, alg_flops, t_s, mode=None, kname=None):
+    """Roofline object for one kernel (or a whole step): the binding resource of max(B/BW, F/peak)."""
+    hbm_peak, hbm_src = measured_peaks()
+    alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
+    alu_src = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")
+    if mode and kname == "kron_fused_tf32x3_kernel":
+        alu_peak, alu_src = MMA_TF32_TFLOPS / 3, "measured mma.sync TF32 (profiles/r01_microbench_mma.jsonl) / 3"
+    t_hbm, t_alu = alg_bytes / (hbm_peak * 1e9), alg_flops / (alu_peak * 1e12)
+    if t_hbm >= t_alu:
+        ach = alg_bytes / t_s / 1e9
+        return {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src}
+    ach = alg_flops / t_s / 1e12
+    return {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
+            "frac": round(ach / alu_peak, 4), "peak_source": alu_src}
+
+
+def measure_single(kron, synth, torch, cfg_name, args, dev, rank, barrier, mode=None, ws=1):
+    """Device-timed kron_matmul steps on one configuration (inputs resident in HBM).  Returns a dict with the
+    step statistics, the dominant kernel's roofline and the whole-step roofline, plus the buffers."""
+    cfg, M, P, Q, dtn = CONFIGS[cfg_name]
+    dt = np.float32 if dtn == "float32" else np.float64
+    tdt = torch.float32 if dt == np.float32 else torch.float64
+    es = 4 if dt == np.float32 else 8
+    seed = synth.SEED_BASE + cfg
+    K, L = int(np.prod(P)), int(np.prod(Q))
+    stream = torch.cuda.current_stream()
+    X = torch.empty((M, K), dtype=tdt, device=dev)
+    synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=rank * M, ld=K)
+    Fs_h = synth.factors(P, Q, seed, "urand", dt)
+    Fs = [torch.from_numpy(f).to(dev) for f in Fs_h]
+    Y = torch.empty((M, L), dtype=tdt, device=dev)
+    tuned = None
+    if args.autotune:
+        # P:599-619: time the candidate plans on these buffers, keep the fastest (untimed, before warm-up)
+        _, ncand, best = kron.autotune(X, Fs, Y, reps=3, mode=mode)
+        tuned = {"candidates": ncand, "best_ms": round(best, 5)}
+    wsz = kron.workspace_size(M, P, Q, tdt, mode)
+    work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
+    plan = kron.plan_describe(M, P, Q, tdt, mode)
+    kernels = kron.plan_kernels(M, P, Q, tdt, mode)
+    npass = len(plan)
+    W = widths(P, Q)
+
+    def mk_events(n):
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        for e in evs:
+            e.record(stream)  # materialise the cudaEvent_t handles
+        return evs
+
+    for _ in range(args.warmup):
+        kron.matmul_ws(X, Fs, Y, work, mode=mode)
+    torch.cuda.synchronize()
+    pass_events = [mk_events(npass + 1) for _ in range(args.steps)]
+    t_start, t_end = mk_events(2)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clocks:
+        t_start.record(stream)
+        for k in range(args.steps):
+            kron.matmul_ws_events(X, Fs, Y, work, [e.cuda_event for e in pass_events[k]], mode=mode)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    ms = t_start.elapsed_time(t_end)
+    if ws > 1:
+        ms = max_over_ranks(ms, dev)
+    fl_step = flops_of(M, P, Q)
+    # per-pass (kernel) timing -> roofline of the dominant kernel; per-step times -> median / min
+    pass_ms = np.zeros(npass)
+    step_ms = []
+    for k in range(args.steps):
+        for i in range(npass):
+            pass_ms[i] += pass_events[k][i].elapsed_time(pass_events[k][i + 1])
+        step_ms.append(pass_events[k][0].elapsed_time(pass_events[k][npass]))
+    pass_ms /= args.steps
+    dom = int(np.argmax(pass_ms))
+    first, nf, kind = plan[dom]
+    w_in, w_out = W[first], W[first - nf]
+    alg_bytes = es * M * (w_in + w_out) + sum(es * P[f - 1] * Q[f - 1] for f in range(first, first - nf, -1))
+    alg_flops = sum(2.0 * M * W[f] * Q[f - 1] for f in range(first, first - nf, -1))
+    kname = kernels[dom]
+    roof = roofline_of(M, P, Q, es, alg_bytes, alg_flops, pass_ms[dom] / 1e3, mode, kname)
+    traffic, tsrc = ncu_traffic(cfg_name if not mode else cfg_name + "_" + mode, kname)
+    roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
+                 "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
+                 "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
+                 "timing": "CUDA events on the launching stream around each launch, mean over the timed steps",
+                 "traffic": traffic, "traffic_source": tsrc})
+    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt, mode)
+    step_roof = roofline_of(M, P, Q, es, b_alg, f_alg, ms / args.steps / 1e3, mode,
+                            "kron_fused_tf32x3_kernel" if mode and "kron_fused_tf32x3_kernel" in kernels else None)
+    hbm_peak, _ = measured_peaks()
+    alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
+    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12))
+    res = {
+        "workload": cfg_name, "dtype": "f32" if es == 4 else "f64", "M": M, "P": P, "Q": Q, "K": K, "L": L,
+        "ms_per_step": round(ms / args.steps, 5), "value": round(ws * fl_step * args.steps / (ms / 1e3) / 1e9, 2),
+        "unit": "GFLOP/s", "steps": args.steps, "warmup": args.warmup, **step_stats(step_ms),
+        "plan": [list(p) for p in plan], "kernels": kernels, "autotune": tuned,
+        "pass_ms": [round(float(v), 5) for v in pass_ms],
+        "roofline": roof,
+        "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof / (ms / args.steps / 1e3), 4),
+                          "bound": step_roof["bound"], "alg_bytes": b_alg, "alg_flops": f_alg},
+        "gpu_launches": npass * args.steps, "clocks": clocks.summary(),
+        "l2": "inputs larger than L2 (no flush)",
+    }
+    return res, (X, Fs_h, Fs, Y, work, seed, dt, tdt, es, M, K, L, fl_step)
+
+
+def cpu_baseline_of(cfg_name, M, P, Q, seed, dt):
+    import oracle
+    cores = oracle.threads(len(os.sched_getaffinity(0)))  # all host cores (torchrun sets OMP_NUM_THREADS=1)
+    rate, rows, t, reps = cpu_oracle_rate(M, P, Q, seed, dt)
+    return {"value": round(rate, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+            "sample": f"rows 0..{rows - 1} of config {cfg_name} (M={M}) x {reps} passes, {t:.1f} s; plain C "
+                      f"fp64 Algorithm 1 (oracle/), OpenMP over rows"}
+
+
+def run_single(args, kron, synth, torch, ws, rank, local, dev, barrier):
+    """N = 1 (or --no-dist under torchrun: row-partitioned weak scaling, no communication)."""
+    mode = args.mode
+    res, bufs = measure_single(kron, synth, torch, args.config, args, dev, rank, barrier, mode, ws)
+    X, Fs_h, Fs, Y, work, seed, dt, tdt, es, M, K, L, fl_step = bufs
+    stream = torch.cuda.current_stream()
+
+    # e2e through the public C-ABI with HOST buffers: kron_matmul_host streams row chunks H2D -> passes ->
+    # D2H with the copies overlapping; the host X is a pinned copy of the device input
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((M, K), dtype=tdt, pin_memory=True)
+        Xh.copy_(X)
+        Fh = [torch.from_numpy(f).pin_memory() for f in Fs_h]
+        Yh = torch.empty((M, L), dtype=tdt, pin_memory=True)
+        del X, Y, work
+        torch.cuda.empty_cache()
+        kron.matmul_host(Xh, Fh, Yh, mode=mode)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            kron.matmul_host(Xh, Fh, Yh, mode=mode)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if ws > 1:
+            ems = max_over_ranks(ems, dev)
+        h2d = M * K * es + sum(f.numel() * es for f in Fh)
+        e2e = {"value": round(ws * fl_step * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(ws * h2d), "d2h_bytes_per_step": int(ws * M * L * es),
+               "steps": args.e2e_steps,
+               "path": "pinned host X,F -> kron_matmul_host (public C-ABI: row-chunk H2D / passes / D2H "
+                       "pipeline) -> pinned host Y"}
+        del Xh, Yh
+    else:
+        del X, Y, work
+    torch.cuda.empty_cache()
+
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        _, Mc, Pc, Qc, _ = CONFIGS[args.config]
+        cpu = cpu_baseline_of(args.config, Mc, Pc, Qc, seed, dt)
+
+    subs = None
+    if ws == 1 and not args.no_subconfigs and not mode:
+        subs = {}
+        for name in SUBCONFIGS:
+            if name == args.config:
+                continue
+            r, b = measure_single(kron, synth, torch, name, args, dev, rank, barrier, None, 1)
+            del b
+            torch.cuda.empty_cache()
+            subs[name] = {k: v for k, v in r.items() if k not in ("steps", "warmup", "l2")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
+            **({"mode": "3xtf32 (fp32 data, TF32 split tensor-core MMAs; reported separately)"} if mode else {}),
+            "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
+            "config": {"workload": args.config, "M_per_gpu": M, "P": res["P"], "Q": res["Q"], "K": K, "L": L,
+                       "plan": res["plan"], "kernels": res["kernels"], "autotune": res["autotune"],
+                       "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
+                       "l2": "inputs larger than L2 (no flush)"},
+            "step_stats": {k: res[k] for k in ("mean_ms", "median_ms", "min_ms", "max_ms")},
+            "pass_ms": res["pass_ms"],
+            "roofline": res["roofline"], "step_roofline": res["step_roofline"],
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": res["gpu_launches"], "clocks": res["clocks"],
+            "configs": subs,
+        }
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_dist(args, kron, synth, torch, ws, rank, local, dev, barrier):
+    """Algorithm 2 through kron_matmul_dist: config E (default) strong-scaled over the paper-rule grid, or
+    a Fig 11 workload weak-scaled (M grows with the GPU count)."""
+    cfg_name = args.config
+    cfg, M, P, Q, dtn = CONFIGS[cfg_name]
+    weak = cfg_name in WEAK
+    if weak:
+        M = M * ws
     dt = np.float32 if dtn == "float32" else np.float64
     tdt = torch.float32 if dt == np.float32 else torch.float64
     es = 4 if dt == np.float32 else 8
     seed = synth.SEED_BASE + cfg
     K, L = int(np.prod(P)), int(np.prod(Q))
     GM, GK = (0, 0) if args.grid is None else (int(v) for v in args.grid.lower().split("x"))
+    share = os.environ.get("KRON_BENCH_SHARE_GPU") == "1"
     if ws == 1:
-        GM, GK = 1, 1
-    if ws > 1:
-        ctx = kron.DistContext(args.exchange, GM=GM, GK=GK)
-    else:
         ctx = kron.DistContext("virtual", GM=1, GK=1)
+    else:
+        backend = args.exchange if not (share and args.exchange == "nccl") else "virtual-unavailable"
+        if backend == "virtual-unavailable":
+            raise SystemExit("NCCL cannot place two ranks on one GPU: use --exchange p2p with KRON_BENCH_SHARE_GPU")
+        ctx = kron.DistContext(backend, GM=GM, GK=GK, chunks=args.chunks)
     gm, gk = ctx.coords(rank)
-    Ml, Kl = M // ctx.GM, K // ctx.GK
+    Ml, Kl, Ll = M // ctx.GM, K // ctx.GK, L // ctx.GK
     stream = torch.cuda.current_stream()
     X = torch.empty((Ml, Kl), dtype=tdt, device=dev)
     synth.fill_device(X.data_ptr(), Ml, Kl, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=gm * Ml,
                       c0=gk * Kl, ld=K)
-    Fs = [torch.from_numpy(f).to(dev) for f in synth.factors(P, Q, seed, "urand", dt)]
-    Y = torch.empty((Ml, L // ctx.GK), dtype=tdt, device=dev)
+    Fs_h = synth.factors(P, Q, seed, "urand", dt)
+    Fs = [torch.from_numpy(f).to(dev) for f in Fs_h]
+    Y = torch.empty((Ml, Ll), dtype=tdt, device=dev)
     xs, ys = (X, Y) if ctx.backend != "virtual" else ([X], [Y])
-    for _ in range(args.warmup):
-        kron.matmul_dist(M, xs, Fs, ctx, out=ys)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
-        t0.record(stream)
-        for _ in range(args.steps):
-            kron.matmul_dist(M, xs, Fs, ctx, out=ys)
-        t1.record(stream)
+
+    def timed(fn, steps):
+        for _ in range(args.warmup):
+            fn()
         torch.cuda.synchronize()
-    barrier()
-    ms = t0.elapsed_time(t1)
+        barrier()
+        torch.cuda.synchronize()
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+        with ClockSampler(local) as clocks:
+            evs[0].record(stream)
+            for k in range(steps):
+                fn()
+                evs[k + 1].record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = evs[0].elapsed_time(evs[-1])
+        step_ms = [evs[k].elapsed_time(evs[k + 1]) for k in range(steps)]
+        if ws > 1:
+            ms = max_over_ranks(ms, dev)
+        return ms, step_ms, clocks.summary()
+
+    ms, step_ms, clk = timed(lambda: kron.matmul_dist(M, xs, Fs, ctx, out=ys), args.steps)
     if ws > 1:
-        ms = max_over_ranks(ms, dev)
+        ctx.sync()  # asynchronous NCCL errors of the timed calls surface here
     rounds, ledger = kron.dist_plan(M, P, Q, ctx.GM, ctx.GK)
     fl_step = flops_of(M, P, Q)
     value = fl_step * args.steps / (ms / 1e3) / 1e9
-    hbm_peak, hbm_src = measured_peaks()
-    alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
     b_alg, f_alg = kron.plan_cost(M, P, Q, tdt)
+    hbm_peak, _ = measured_peaks()
+    alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
     t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12)) / ws
+    round_info = ctx.round_info(M, P, Q, tdt) if ctx.GK > 1 else []
+
+    # e2e: this rank's block from pinned host memory -> kron_matmul_dist -> Y_local back to pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        Xh = torch.empty((Ml, Kl), dtype=tdt, pin_memory=True)
+        Xh.copy_(X)
+        Yh = torch.empty((Ml, Ll), dtype=tdt, pin_memory=True)
+
+        def e2e_step():
+            X.copy_(Xh, non_blocking=True)
+            kron.matmul_dist(M, xs, Fs, ctx, out=ys)
+            Yh.copy_(Y, non_blocking=True)
+
+        ems, _, _ = timed(e2e_step, args.e2e_steps)
+        e2e = {"value": round(fl_step * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(M * K * es), "d2h_bytes_per_step": int(M * L * es), "steps": args.e2e_steps,
+               "path": "per rank: pinned host X block -> H2D -> kron_matmul_dist -> D2H of Y_local (all ranks' bytes)"}
+
+    # secondary: the same rows on a row-only grid {G,1} (no exchange, P:706-708)
+    row_only = None
+    if ws > 1 and ctx.GK > 1 and not args.no_row_only and args.exchange == "nccl" and not share:
+        ctx2 = kron.DistContext("nccl", GM=ws, GK=1)
+        Mr = M // ws
+        X2 = torch.empty((Mr, K), dtype=tdt, device=dev)
+        synth.fill_device(X2.data_ptr(), Mr, K, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=rank * Mr, ld=K)
+        Y2 = torch.empty((Mr, L), dtype=tdt, device=dev)
+        del X, Y
+        torch.cuda.empty_cache()
+        ms2, step2, clk2 = timed(lambda: kron.matmul_dist(M, X2, Fs, ctx2, out=Y2), args.steps)
+        row_only = {"grid": [ws, 1], "value": round(fl_step * args.steps / (ms2 / 1e3) / 1e9, 2), "unit": "GFLOP/s",
+                    "ms_per_step": round(ms2 / args.steps, 5), **step_stats(step2), "clocks": clk2}
+        ctx2.close()
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
+            "scaling": "weak" if weak else "strong", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
             "data": "synthetic (seeded counter-based U[0,1), each rank generates its own block in HBM)",
-            "config": {"workload": args.config, "M": M, "P": P, "Q": Q, "grid": [ctx.GM, ctx.GK],
+            "config": {"workload": cfg_name, "M": M, "P": P, "Q": Q, "grid": [ctx.GM, ctx.GK],
                        "rounds": rounds, "exchanged_values_per_step": int(sum(ledger)),
+                       "fused_layout_per_round": round_info, "row_chunks": args.chunks,
                        "parallelism": f"Algorithm 2 grid {ctx.GM}x{ctx.GK} (rows x K), " +
-                                      ("NCCL all-to-all" if args.exchange == "nccl" else
-                                       "P2P pull kernel over peer memory (CUDA IPC)"),
+                                      ("NCCL all-to-all" if ctx.backend == "nccl" else
+                                       "P2P over peer memory (CUDA IPC)" if ctx.backend == "p2p" else
+                                       "single GPU (grid 1x1)"),
                        "l2": "inputs larger than L2 (no flush)"},
+            "step_stats": step_stats(step_ms),
             "step_roofline": {"t_roof_ms_per_gpu": round(t_roof * 1e3, 4),
                               "frac": round(t_roof / (ms / args.steps / 1e3), 4)},
-            "gpu_launches": None, "clocks": clocks.summary(),
+            "e2e": e2e, "row_only": row_only,
+            "gpu_launches": None, "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     ctx.close()
-    if ws > 1:
-        torch.distributed.destroy_process_group()
     return 0
 
 
@@ -381,18 +665,20 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)  # the paper: "average of 100 runs after 10 warm-ups"
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="B", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="E", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--dist", action="store_true",
-                    help="distributed Algorithm 2 (kron_matmul_dist over NCCL): the configuration's M rows are "
-                         "split over a {GM,GK} grid (strong scaling); default grid = paper rule")
+    ap.add_argument("--no-subconfigs", action="store_true", help="N = 1: skip the B/C32/C64/D1/D2 sub-lines")
+    ap.add_argument("--no-row-only", action="store_true", help="N > 1: skip the row-only {G,1} secondary line")
+    ap.add_argument("--dist", action=argparse.BooleanOptionalAction, default=None,
+                    help="Algorithm 2 through kron_matmul_dist (default: on for N > 1, off for N = 1)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
-                    help="--dist exchange: ncclAlltoAll (pack / all-to-all / StoreGPUTile) or the one-kernel "
-                         "P2P pull over peer memory (NEXT-1, P:652)")
-    ap.add_argument("--grid", default=None, help="GMxGK for --dist (e.g. 8x1 row-only, 4x2 paper rule)")
+                    help="distributed exchange: ncclAlltoAll (fused send / receive layouts) or the P2P push / pull "
+                         "kernels over peer memory (NEXT-1, P:652)")
+    ap.add_argument("--grid", default=None, help="GMxGK for the distributed path (default: the paper rule)")
+    ap.add_argument("--chunks", type=int, default=2, help="row chunks per round (exchange / compute overlap)")
     ap.add_argument("--mode", default=None, choices=["3xtf32"],
                     help="fp32 configs only: the separately reported 3xTF32 tensor-core mode (NEXT-4)")
     ap.add_argument("--autotune", action=argparse.BooleanOptionalAction, default=True,
@@ -404,7 +690,7 @@ def main():
         ap.error("--warmup must be >= 3")
 
     if args.impl == "reference":
-        return run_reference(args, args.config)
+        return run_reference(args, args.config if args.config not in WEAK else "E")
     if args.sweep:
         return run_sweep(args)
 
@@ -434,168 +720,15 @@ def main():
         if ws > 1:
             torch.distributed.barrier()
 
-    if args.dist:
-        return run_dist(args, ws, rank, local, dev, barrier)
-
-    cfg, M, P, Q, dtn = CONFIGS[args.config]
-    dt = np.float32 if dtn == "float32" else np.float64
-    mode = args.mode
-    if mode and dt != np.float32:
+    use_dist = args.dist if args.dist is not None else (ws > 1 or args.config in WEAK)
+    if args.mode and use_dist:
+        ap.error("--mode 3xtf32 is a single-GPU mode")
+    if args.mode and CONFIGS[args.config][4] != "float32":
         ap.error("--mode 3xtf32 applies to the fp32 configs (B, C32, E)")
-    tdt = torch.float32 if dt == np.float32 else torch.float64
-    es = 4 if dt == np.float32 else 8
-    seed = synth.SEED_BASE + cfg
-    K, L = int(np.prod(P)), int(np.prod(Q))
-    stream = torch.cuda.current_stream()
-
-    # inputs resident in HBM: this rank's block of rows of a (ws*M) x K matrix
-    X = torch.empty((M, K), dtype=tdt, device=dev)
-    synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", dt, stream=stream.cuda_stream, r0=rank * M, ld=K)
-    Fs_h = synth.factors(P, Q, seed, "urand", dt)
-    Fs = [torch.from_numpy(f).to(dev) for f in Fs_h]
-    Y = torch.empty((M, L), dtype=tdt, device=dev)
-    tuned = None
-    if args.autotune:
-        # time the candidate plans on these buffers, keep the fastest (untimed, before warm-up)
-        _, ncand, best = kron.autotune(X, Fs, Y, reps=3, mode=mode)
-        tuned = {"candidates": ncand, "best_ms": round(best, 5)}
-    wsz = kron.workspace_size(M, P, Q, tdt, mode)
-    work = torch.empty(max(wsz, 1), dtype=torch.uint8, device=dev)
-    plan = kron.plan_describe(M, P, Q, tdt, mode)
-    npass = len(plan)
-    W = widths(P, Q)
-
-    def mk_events(n):
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
-        for e in evs:
-            e.record(stream)  # materialise the cudaEvent_t handles
-        return evs
-
-    for _ in range(args.warmup):
-        kron.matmul_ws(X, Fs, Y, work, mode=mode)
-    torch.cuda.synchronize()
-
-    pass_events = [mk_events(npass + 1) for _ in range(args.steps)]
-    t_start, t_end = mk_events(2)
-    torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        t_start.record(stream)
-        for k in range(args.steps):
-            kron.matmul_ws_events(X, Fs, Y, work, [e.cuda_event for e in pass_events[k]], mode=mode)
-        t_end.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    torch.cuda.synchronize()
-    ms = t_start.elapsed_time(t_end)
-    if ws > 1:
-        ms = max_over_ranks(ms, dev)
-    fl_step = flops_of(M, P, Q)
-    value = ws * fl_step * args.steps / (ms / 1e3) / 1e9  # whole-job GFLOP/s
-
-    # per-pass (kernel) timing -> roofline of the dominant kernel
-    pass_ms = np.zeros(npass)
-    for k in range(args.steps):
-        for i in range(npass):
-            pass_ms[i] += pass_events[k][i].elapsed_time(pass_events[k][i + 1])
-    pass_ms /= args.steps
-    dom = int(np.argmax(pass_ms))
-    first, nf, kind = plan[dom]
-    w_in, w_out = W[first], W[first - nf]
-    alg_bytes = es * M * (w_in + w_out) + sum(es * P[f - 1] * Q[f - 1] for f in range(first, first - nf, -1))
-    alg_flops = sum(2.0 * M * W[f] * Q[f - 1] for f in range(first, first - nf, -1))
-    hbm_peak, hbm_src = measured_peaks()
-    alu_peak = FP32_PEAK_TFLOPS if dt == np.float32 else FP64_PEAK_TFLOPS
-    alu_src = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")
-    if mode and kron.plan_kernels(M, P, Q, tdt, mode)[dom] == "kron_fused_tf32x3_kernel":
-        # the 3xTF32 pass runs on the warp MMA: measured mma.sync TF32 rate / 3 MMAs per product
-        alu_peak, alu_src = MMA_TF32_TFLOPS / 3, "measured mma.sync TF32 (profiles/r01_microbench_mma.jsonl) / 3"
-    t_dom = pass_ms[dom] / 1e3
-    t_hbm, t_alu = alg_bytes / (hbm_peak * 1e9), alg_flops / (alu_peak * 1e12)
-    if t_hbm >= t_alu:
-        ach = alg_bytes / t_dom / 1e9
-        roof = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(ach / hbm_peak, 4), "peak_source": hbm_src}
-    else:
-        ach = alg_flops / t_dom / 1e12
-        roof = {"bound": "alu", "achieved": round(ach, 3), "peak": round(alu_peak, 2), "unit": "TFLOP/s",
-                "frac": round(ach / alu_peak, 4),
-                "peak_source": alu_src}
-    kname = kron.plan_kernels(M, P, Q, tdt, mode)[dom]
-    roof.update({"kernel": f"{kname} (pass {dom}: factors {first}..{first - nf + 1}, {kind})",
-                 "ms_per_launch": round(float(pass_ms[dom]), 5), "alg_bytes_per_launch": int(alg_bytes),
-                 "alg_flops_per_launch": alg_flops, "share_of_step": round(float(pass_ms[dom] / (ms / args.steps)), 4),
-                 "traffic": ncu_traffic(args.config, kname)})
-
-    # whole-step roofline (all passes): T_roof = max(B_alg/BW, F_alg/peak)
-    b_alg, f_alg = kron.plan_cost(M, P, Q, tdt, mode)
-    t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12))
-    step_frac = t_roof / (ms / args.steps / 1e3)
-
-    # e2e through the public API with host buffers: H2D of X and F, kron_matmul, D2H of Y
-    e2e = None
-    if not args.no_e2e:
-        Xh = torch.empty((M, K), dtype=tdt, pin_memory=True)
-        Xh.numpy().reshape(-1)[:] = synth.fill(M * K, seed, 0, "urand", dt, first=rank * M * K)
-        Fh = [torch.from_numpy(f).pin_memory() for f in Fs_h]
-        Yh = torch.empty((M, L), dtype=tdt, pin_memory=True)
-        del X
-        torch.cuda.empty_cache()
-
-        def e2e_step():
-            # kron_matmul_host: row chunks stream H2D -> passes -> D2H with the copies overlapping
-            kron.matmul_host(Xh, Fh, Yh, mode=mode)
-
-        e2e_step()
-        torch.cuda.synchronize()
-        e0, e1 = mk_events(2)
-        barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        for _ in range(args.e2e_steps):
-            e2e_step()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        ems = e0.elapsed_time(e1)
-        if ws > 1:
-            ems = max_over_ranks(ems, dev)
-        h2d = M * K * es + sum(f.numel() * es for f in Fh)
-        e2e = {"value": round(ws * fl_step * args.e2e_steps / (ems / 1e3) / 1e9, 3), "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(M * L * es), "steps": args.e2e_steps,
-               "path": "pinned host X,F -> kron_matmul_host (public C-ABI: row-chunk H2D / passes / D2H "
-                       "pipeline) -> pinned host Y"}
-
-    cpu = None
-    if rank == 0 and not args.no_cpu:
-        import oracle
-        cores = oracle.threads(len(os.sched_getaffinity(0)))  # all host cores (torchrun sets OMP_NUM_THREADS=1)
-        rate, rows, t, reps = cpu_oracle_rate(M, P, Q, seed, dt)
-        cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
-               "sample": f"rows 0..{rows - 1} of config {args.config} (M={M}) x {reps} passes, {t:.1f} s; plain C "
-                         f"fp64 Algorithm 1 (oracle/), OpenMP over rows"}
-
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": round(value, 2), "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 5), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32" if es == 4 else "f64",
-            **({"mode": "3xtf32 (fp32 data, TF32 split tensor-core MMAs; reported separately)"} if mode else {}),
-            "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
-            "config": {"workload": args.config, "M_per_gpu": M, "P": P, "Q": Q, "K": K, "L": L,
-                       "plan": [list(p) for p in plan], "kernels": kron.plan_kernels(M, P, Q, tdt, mode), "autotune": tuned,
-                       "parallelism": "single GPU" if ws == 1 else f"row partition x{ws} (no communication)",
-                       "l2": "inputs larger than L2 (no flush)"},
-            "roofline": roof,
-            "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(step_frac, 4),
-                              "alg_bytes": b_alg, "alg_flops": f_alg},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": npass * args.steps,
-            "clocks": clocks.summary(),
-        }
-        print(json.dumps(line), flush=True)
+    rc = (run_dist if use_dist else run_single)(args, kron, synth, torch, ws, rank, local, dev, barrier)
     if ws > 1:
         torch.distributed.destroy_process_group()
-    return 0
+    return rc
 
 
 if __name__ == "__main__":

@@ -164,9 +164,19 @@ kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32
  *     0  NCCL: `nccl_unique_id` points to the 128-byte ncclUniqueId created by rank 0 and
  *        broadcast by the caller (e.g. over a torch ProcessGroup); world_size = GM*GK ranks,
  *        one per GPU; `rank` is this process's rank.  The row-group communicator is
- *        ncclCommSplit(world, color = gM, key = gK).
+ *        ncclCommSplit(world, color = gM, key = gK).  Per round and per row chunk (rows are
+ *        independent): the local passes, whose LAST pass writes the destination-major
+ *        send block send[d][rows][W'/GK] directly from its epilogue where the kernel has one (the
+ *        fp32 16x16 cluster kernel and the fp32 16x16 / 32x32 chunk-pair kernels; else a pack
+ *        kernel); ONE ncclAlltoAll on the context's own stream, so chunk c's exchange overlaps chunk
+ *        c+1's passes; and StoreGPUTile (line 685), which the NEXT round's first pass performs
+ *        itself by reading the receive buffer through a 5-D tensor map in StoreGPUTile order (any
+ *        fused kernel but the 64x32 pair; else a remap kernel).  After the last round one remap
+ *        kernel writes Y_local.  Every value crosses HBM once per round at the source and once at the
+ *        destination besides the local passes' own traffic.
  *     1  virtual: ONE process drives all GM*GK ranks on the current device; the exchange is a
- *        device-to-device copy (used to test the distributed data path on a single GPU).
+ *        device-to-device copy (used to test the distributed data path on a single GPU) and the
+ *        rounds use exactly backend 0's buffers, chunks, fused send / receive layouts and kernels.
  *        nccl_unique_id and rank are ignored.
  *     2  P2P (peer memory, "a single CUDA kernel ... when GPUs support P2P"): one rank per
  *        process (`rank` = this process's rank, nccl_unique_id ignored).  Before the first call the
@@ -174,19 +184,41 @@ kron_status_t kron_plan_cost(int64_t M, int32_t N, const int32_t *P, const int32
  *        handles (e.g. all_gather over a torch ProcessGroup) and map the row-group peers' heaps
  *        (kron_dist_p2p_connect).  A round whose last local pass is the fp32 16x16 cluster kernel or
  *        an fp32 16x16 / 32x32 chunk-pair kernel (and that is not the last round) FUSES the exchange
- *        into that pass: its store warps write
- *        every value straight into its StoreGPUTile position in the destination rank's heap (peer
- *        stores over NVLink / NVSwitch), between two device-side flag barriers.  Every other round
- *        writes its local output into this rank's heap, meets the row group at a flag barrier, and
- *        runs ONE pull kernel that reads every value it owns straight from the peers' heaps into its
- *        StoreGPUTile position — the pack, the all-to-all and StoreGPUTile of backend 0 in one pass.
- *        Ranks may share a GPU (IPC within one device), which is how it is tested on one B200.
+ *        into that pass: its store warps write every value straight into its StoreGPUTile position
+ *        in the destination rank's heap (peer stores over NVLink / NVSwitch), between two
+ *        device-side flag barriers (the round's earlier passes run before the first barrier).  Every
+ *        other round writes its local output into this rank's heap, meets the row group at a flag
+ *        barrier, and runs ONE pull kernel that reads every value it owns straight from the peers'
+ *        heaps into its StoreGPUTile position.  Ranks may share a GPU (IPC within one device), which
+ *        is how it is tested on one B200.  Whether rounds push is fixed at context creation
+ *        (KRON_P2P_NO_PUSH in the environment then, or kron_dist_ctx_set) so all ranks agree.
  * GM = GK = 0 selects the grid by the paper's rule.                               */
 typedef struct kron_dist_ctx kron_dist_ctx_t;
 
 kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, int32_t world_size,
                                    int32_t rank, int32_t GM, int32_t GK, kron_dist_ctx_t **out);
 kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx);
+/* Context options (host only; set the same value on every rank before the calls that use it):
+ *   KRON_DIST_OPT_CHUNKS        row chunks per round, 1..64 (backends 0 / 1; default 2)
+ *   KRON_DIST_OPT_FUSED_LAYOUT  0 / 1: fused send / receive layouts (backends 0 / 1; default 1 — 0 forces
+ *                               the separate pack and remap kernels, for testing)
+ *   KRON_DIST_OPT_P2P_PUSH      0 / 1: backend 2's fused push rounds (default 1 unless KRON_P2P_NO_PUSH
+ *                               was set when the context was created)
+ * Errors: null ctx, unknown option or value out of range -> KRON_ERR_INVALID_ARG. */
+enum { KRON_DIST_OPT_CHUNKS = 1, KRON_DIST_OPT_FUSED_LAYOUT = 2, KRON_DIST_OPT_P2P_PUSH = 3 };
+kron_status_t kron_dist_ctx_set(kron_dist_ctx_t *ctx, int32_t option, int32_t value);
+/* Wait (host) until `stream` has drained, polling the context's asynchronous errors meanwhile:
+ * NCCL (ncclCommGetAsyncError) -> KRON_ERR_NCCL; still not done after timeout_ms (< 0: no bound)
+ * -> KRON_ERR_NCCL for backend 0 (its communicators are aborted: the context is unusable) or
+ * KRON_ERR_CUDA otherwise; a P2P barrier that gave up (kron_dist_p2p_timeouts) -> KRON_ERR_CUDA.
+ * kron_matmul_dist itself never blocks; it returns KRON_ERR_NCCL up front when an earlier
+ * collective of the context failed. */
+kron_status_t kron_dist_sync(kron_dist_ctx_t *ctx, void *stream, int32_t timeout_ms);
+/* Per round (host only, up to `cap`): whether backends 0 / 1 write the send buffer from the last
+ * pass (fused_send[j]) and read the receive buffer in place in the first pass (fused_recv[j]). */
+kron_status_t kron_dist_round_info(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                   const kron_dist_ctx_t *ctx, int32_t cap, int32_t *nrounds, int32_t *fused_send,
+                                   int32_t *fused_recv);
 /* Grid actually used by the context. */
 kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_t *GK);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */

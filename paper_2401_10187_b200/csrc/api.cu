@@ -173,25 +173,28 @@ kron_status_t cuda_fail(int err, const char *what) {
 }
 
 kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
-                       void *const *events = nullptr, const PushArgs *push = nullptr) {
+                       void *const *events = nullptr, const PushArgs *push = nullptr, const InRemap *rin = nullptr,
+                       int i0 = 0, int i1 = -1) {
   const size_t es = es_of(plan.dtype);
+  const int np = (int)plan.passes.size();
+  if (i1 < 0 || i1 > np) i1 = np;
   int ip = 0;
   void *bufs[4] = {const_cast<void *>(X), Y, ws,
                    ws ? static_cast<char *>(ws) + (size_t)plan.ws_elems * es : nullptr};
-  for (const PassPlan &pp : plan.passes) {
+  for (int i = i0; i < i1; ++i) {
+    const PassPlan &pp = plan.passes[i];
     const void *in = bufs[pp.src];
     void *out = bufs[pp.dst];
     int err = 0;
     if (events && cudaEventRecord((cudaEvent_t)events[ip], (cudaStream_t)stream) != cudaSuccess) return KRON_ERR_CUDA;
     ++ip;
+    const bool lastp = i == np - 1, firstp = i == 0;
     if (pp.kind == KIND_FUSED) {
       if (!tmap_available()) return KRON_ERR_CUDA;
-      const void *grp[2 * kMaxFused];
-      const int nfac = pp.pair ? 2 * pp.nf : pp.nf;
-      for (int i = 0; i < nfac; ++i) grp[i] = F[pp.first - 1 - i];
-      void *aux = ws ? static_cast<char *>(ws) + (size_t)plan.nws * plan.ws_elems * es : nullptr;
-      const bool lastp = &pp == &plan.passes.back();
-      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, aux, stream, lastp ? push : nullptr);
+      const void *grp[kMaxFused];
+      for (int k = 0; k < pp.nf; ++k) grp[k] = F[pp.first - 1 - k];
+      err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, stream, lastp ? push : nullptr,
+                         firstp ? rin : nullptr);
     } else if (pp.kind == KIND_GEMM) {
       err = launch_gemm(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
     } else {
@@ -206,7 +209,7 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
 }
 
 size_t ws_bytes_of(const Plan &plan) {
-  return (size_t)plan.nws * (size_t)plan.ws_elems * (size_t)es_of(plan.dtype) + (size_t)plan.aux_bytes;
+  return (size_t)plan.nws * (size_t)plan.ws_elems * (size_t)es_of(plan.dtype);
 }
 
 }  // namespace
@@ -230,16 +233,39 @@ void keep_pool_cached() {
 size_t plan_ws_bytes(const Plan &plan) { return ws_bytes_of(plan); }
 
 kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
-                       const PushArgs *push) {
-  return run_plan(plan, X, F, Y, ws, stream, nullptr, push);
+                       const PushArgs *push, const InRemap *rin, int i0, int i1) {
+  if ((push && push->on && !plan_push_ok(plan, *push)) || (rin && rin->on && !plan_remap_ok(plan, *rin)))
+    return KRON_ERR_UNSUPPORTED;
+  return run_plan(plan, X, F, Y, ws, stream, nullptr, push, rin, i0, i1);
 }
 
-bool plan_push_ok(const Plan &plan) {
-  if (plan.passes.empty()) return false;
+// The pushing epilogues exist in the v9 cluster kernel (16-byte runs: rho, B and the row width must keep
+// every float4 inside one run and 16-byte aligned) and the v6 fp32 chunk-pair kernels (scalar stores).
+bool plan_push_ok(const Plan &plan, const PushArgs &push) {
+  if (plan.passes.empty() || push.GK < 1 || push.GK > kMaxPush || push.B < 1 || push.rho < 1) return false;
   const PassPlan &pp = plan.passes.back();
-  if (pp.kind != KIND_FUSED || pp.pair) return false;
+  if (pp.kind != KIND_FUSED) return false;
+  if (pp.W_out % push.B || push.B % push.rho || pp.W_out / push.B > kMaxPush) return false;
   const FusedInstance &fi = fused_instance(pp.variant);
-  return fi.warp == 10 || (fi.warp == 6 && fi.dtype == KRON_F32 && (fi.P == 16 || fi.P == 32));
+  if (fi.warp == 10) return push.rho % 4 == 0 && push.B % 4 == 0 && push.wd % 4 == 0;
+  return fi.warp == 6 && fi.dtype == KRON_F32 && (fi.P == 16 || fi.P == 32);
+}
+
+// The remapped input view needs every TMA box of the first pass to cover whole runs of rho elements, or
+// lie inside one: fused kernels with the standard 3-D line-box loads (all but v7), rho a multiple of a
+// 128-byte line.
+bool plan_remap_ok(const Plan &plan, const InRemap &rin) {
+  if (plan.passes.empty() || rin.GK < 1 || rin.rho < 1) return false;
+  const PassPlan &pp = plan.passes.front();
+  if (pp.kind != KIND_FUSED || fused_instance(pp.variant).warp == 7) return false;
+  const int64_t line = 128 / es_of(plan.dtype);
+  if (rin.rho % line || pp.W_in % (rin.rho * rin.GK)) return false;
+  const int64_t rl = rin.rho / line, bl = fused_box_lines(pp, plan.dtype);
+  if (bl < 1) return false;
+  if (bl <= rl) return rl % bl == 0;
+  if (bl % rl) return false;
+  const int64_t nr = bl / rl;
+  return nr <= rin.GK ? rin.GK % nr == 0 : nr % rin.GK == 0;
 }
 
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
@@ -375,41 +401,6 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     pp.variant = (pp.kind == KIND_GEMM && dtype == KRON_F64 && policy.dmma && p % 16 == 0 && q % 16 == 0) ? 1 : 0;
     plan->passes.push_back(pp);
     f -= 1;
-  }
-
-  // L2-fused pairs (experimental): two consecutive factor-pipeline passes over the same width run as ONE cooperative
-  // launch; the first pass streams rows into a ring of NR rows that stays in L2 and the second pass
-  // consumes them a few rows behind, so the intermediate does not make an HBM round trip.
-  // Opt-in (KRON_PAIR=1): measured slower than two passes on config B in round 1 (each pass gets half an
-  // SM and the row hand-off polls), although the ring does keep ~60% of the intermediate out of HBM.
-  plan->aux_bytes = 0;
-  if (getenv("KRON_PAIR")) {
-    for (size_t i = 0; i + 1 < plan->passes.size(); ++i) {
-      const PassPlan &A = plan->passes[i], &B = plan->passes[i + 1];
-      if (A.kind != KIND_FUSED || B.kind != KIND_FUSED || fused_instance(A.variant).warp != 2 ||
-          fused_instance(B.variant).warp != 2 || A.nf != B.nf || A.P != B.P || A.W_in != B.W_in)
-        continue;
-      const int ip = fused_find(dtype, A.P, 4);
-      if (ip < 0) continue;
-      PassPlan pp;
-      if (!fused_geometry(fused_instance(ip), A.nf, A.W_in, Mp, &pp)) continue;
-      const int64_t es = es_of(dtype), row_bytes = A.W_in * es;
-      int64_t nr = (48ll << 20) / row_bytes;
-      if (nr > 32) nr = 32;
-      if (nr > M) nr = M;
-      if (nr < 4 || M < 2 * nr) continue;
-      pp.variant = ip;
-      pp.pair = 1;
-      pp.ring_rows = (int)nr;
-      pp.first = A.first;
-      pp.nf = A.nf;
-      pp.W_in = A.W_in;
-      pp.W_out = B.W_out;
-      plan->passes[i] = pp;
-      plan->passes.erase(plan->passes.begin() + i + 1);
-      plan->aux_bytes = nr * row_bytes + 2 * M * (int64_t)sizeof(int);
-      break;  // one ring per plan
-    }
   }
 
   // buffers (Alg 1, 318): the last pass writes Y, X is never written; interior
@@ -814,7 +805,7 @@ kron_status_t kron_plan_describe(int64_t M, int32_t N, const int32_t *P, const i
   *npasses = (int32_t)plan.passes.size();
   for (int i = 0; i < (int)plan.passes.size() && i < cap; ++i) {
     if (first) first[i] = plan.passes[i].first;
-    if (nfactors) nfactors[i] = plan.passes[i].pair ? 2 * plan.passes[i].nf : plan.passes[i].nf;
+    if (nfactors) nfactors[i] = plan.passes[i].nf;
     if (kind) kind[i] = plan.passes[i].kind;
   }
   return KRON_OK;

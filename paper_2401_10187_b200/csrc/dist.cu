@@ -20,9 +20,12 @@
 #include <nccl.h>
 
 #include <algorithm>
-#include <type_traits>
+#include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <thread>
+#include <type_traits>
 #include <vector>
 
 #include "kron_internal.h"
@@ -281,6 +284,7 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
   bool ok = false;
 };
 NcclApi g_nccl;
@@ -305,6 +309,7 @@ const NcclApi &nccl() {
     KRON_SYM(GroupEnd, "ncclGroupEnd");
     KRON_SYM(Send, "ncclSend");
     KRON_SYM(Recv, "ncclRecv");
+    KRON_SYM(CommAbort, "ncclCommAbort");
 #undef KRON_SYM
     g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommSplit && g_nccl.CommDestroy &&
                 (g_nccl.AlltoAll || (g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.Send && g_nccl.Recv));
@@ -320,7 +325,15 @@ using namespace kron;
 struct kron_dist_ctx {
   int backend = 0;  // 0 NCCL, 1 virtual, 2 P2P (peer memory)
   int world = 1, rank = 0, GM = 1, GK = 1, gM = 0, gK = 0;
+  // backends 0 / 1: row chunks per round (chunk c's all-to-all overlaps chunk c+1's local passes) and the
+  // fused data layout (the round's last pass writes the send buffer, the next round's first pass reads the
+  // receive buffer through the StoreGPUTile-ordered tensor map)
+  int nchunks = 2;
+  bool fused = true;
+  bool push = true;  // backend 2: fuse the exchange into the round's last pass where the kernel has a push epilogue
   ncclComm_t world_comm = nullptr, row_comm = nullptr;
+  cudaStream_t comm = nullptr;  // backend 0: all-to-all stream (created on first use on the calling device)
+  std::vector<cudaEvent_t> ev;  // backend 0: [start | per chunk: computed, exchanged]
   // backend 2: symmetric heap = [flags: u64 per row-group peer | timeout word] [out half 0] [out half 1]
   char *heap = nullptr;
   size_t heap_bytes = 0;                 // usable bytes (both halves)
@@ -351,9 +364,34 @@ kron_status_t exchange_nccl(kron_dist_ctx *ctx, int dtype, const void *send, voi
   return KRON_OK;
 }
 
+// asynchronous NCCL errors of earlier calls on this context (non-blocking)
+kron_status_t nccl_async_status(kron_dist_ctx *ctx) {
+  if (ctx->backend != 0) return KRON_OK;
+  const NcclApi &api = nccl();
+  if (!api.CommGetAsyncError) return KRON_OK;
+  for (ncclComm_t c : {ctx->world_comm, ctx->row_comm}) {
+    if (!c) continue;
+    ncclResult_t r = ncclSuccess;
+    if (api.CommGetAsyncError(c, &r) != ncclSuccess || (r != ncclSuccess && r != ncclInProgress)) return KRON_ERR_NCCL;
+  }
+  return KRON_OK;
+}
+
 struct RankBufs {
   void *cur = nullptr, *out = nullptr, *send = nullptr, *recv = nullptr, *ws = nullptr;
 };
+
+// One round of Algorithm 2 (lines 670-692): `k` factors applied locally to the [rows][wl_in] block.
+struct RoundPlan {
+  Plan plan[2];  // [0]: full row chunk, [1]: the ragged last chunk
+  int first = 0, k = 0;
+  int64_t wl_in = 0, wl_out = 0, rho = 0;
+  bool fpush = false;   // backends 0/1: the last pass writes the destination-major send buffer
+  bool fremap = false;  // backends 0/1: the first pass reads the previous round's receive buffer in place
+};
+
+inline char *at(void *p, int64_t elems, size_t es) { return static_cast<char *>(p) + (size_t)elems * es; }
+inline const char *at(const void *p, int64_t elems, size_t es) { return static_cast<const char *>(p) + (size_t)elems * es; }
 
 }  // namespace
 }  // namespace kron
@@ -401,6 +439,8 @@ kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, 
   ctx->world = world_size;
   ctx->GM = GM;
   ctx->GK = GK;
+  // the P2P push mode is fixed here, once (every rank of a context must use the same protocol)
+  ctx->push = getenv("KRON_P2P_NO_PUSH") == nullptr;
   if (backend == 0) {
     if (!nccl_unique_id || rank < 0 || rank >= world_size) {
       delete ctx;
@@ -436,6 +476,19 @@ kron_status_t kron_dist_ctx_create(int32_t backend, const void *nccl_unique_id, 
   return KRON_OK;
 }
 
+kron_status_t kron_dist_ctx_set(kron_dist_ctx_t *ctx, int32_t option, int32_t value) {
+  if (!ctx) return KRON_ERR_INVALID_ARG;
+  switch (option) {
+    case KRON_DIST_OPT_CHUNKS:
+      if (value < 1 || value > 64) return KRON_ERR_INVALID_ARG;
+      ctx->nchunks = value;
+      return KRON_OK;
+    case KRON_DIST_OPT_FUSED_LAYOUT: ctx->fused = value != 0; return KRON_OK;
+    case KRON_DIST_OPT_P2P_PUSH: ctx->push = value != 0; return KRON_OK;
+  }
+  return KRON_ERR_INVALID_ARG;
+}
+
 static void p2p_release(kron_dist_ctx_t *ctx) {
   for (int g = 0; g < ctx->GK && g < kMaxPeers; ++g) {
     if (ctx->peer_heap[g] && ctx->peer_heap[g] != ctx->heap) cudaIpcCloseMemHandle(ctx->peer_heap[g]);
@@ -449,6 +502,11 @@ static void p2p_release(kron_dist_ctx_t *ctx) {
 
 kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx) {
   if (!ctx) return KRON_OK;
+  if (ctx->comm) {
+    cudaStreamSynchronize(ctx->comm);
+    cudaStreamDestroy(ctx->comm);
+  }
+  for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
   if (ctx->backend == 0) {
     const NcclApi &api = nccl();
     if (ctx->row_comm) api.CommDestroy(ctx->row_comm);
@@ -457,6 +515,50 @@ kron_status_t kron_dist_ctx_destroy(kron_dist_ctx_t *ctx) {
   if (ctx->backend == 2) p2p_release(ctx);
   delete ctx;
   return KRON_OK;
+}
+
+kron_status_t kron_dist_sync(kron_dist_ctx_t *ctx, void *stream, int32_t timeout_ms) {
+  if (!ctx) return KRON_ERR_INVALID_ARG;
+  cudaEvent_t done;
+  if (cudaEventCreateWithFlags(&done, cudaEventDisableTiming) != cudaSuccess) return KRON_ERR_CUDA;
+  if (cudaEventRecord(done, (cudaStream_t)stream) != cudaSuccess) {
+    cudaEventDestroy(done);
+    return KRON_ERR_CUDA;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  kron_status_t st = KRON_OK;
+  for (unsigned sleep_us = 10;; sleep_us = std::min(sleep_us * 2, 2000u)) {
+    const cudaError_t q = cudaEventQuery(done);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) {
+      st = KRON_ERR_CUDA;
+      break;
+    }
+    if ((st = nccl_async_status(ctx)) != KRON_OK) break;
+    const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_ms >= 0 && ms > timeout_ms) {
+      st = ctx->backend == 0 ? KRON_ERR_NCCL : KRON_ERR_CUDA;
+      break;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(sleep_us));
+  }
+  if (st == KRON_OK) st = nccl_async_status(ctx);
+  if (st == KRON_OK && ctx->backend == 2 && ctx->heap) {
+    uint32_t to = 0;
+    if (cudaMemcpy(&to, ctx->heap + kP2PTimeoutOff, sizeof(to), cudaMemcpyDeviceToHost) != cudaSuccess) st = KRON_ERR_CUDA;
+    else if (to) st = KRON_ERR_CUDA;  // a barrier gave up: the result is not trustworthy
+  }
+  if (st == KRON_ERR_NCCL && ctx->backend == 0) {
+    // a stuck or failed collective: abort the communicators so the stream drains (the context is unusable)
+    const NcclApi &api = nccl();
+    if (api.CommAbort) {
+      if (ctx->row_comm) api.CommAbort(ctx->row_comm);
+      if (ctx->world_comm) api.CommAbort(ctx->world_comm);
+      ctx->row_comm = ctx->world_comm = nullptr;
+    }
+  }
+  cudaEventDestroy(done);
+  return st;
 }
 
 kron_status_t kron_dist_p2p_heap_bytes(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
@@ -542,6 +644,123 @@ kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_
   return KRON_OK;
 }
 
+kron_status_t kron_dist_round_info(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                   const kron_dist_ctx_t *ctx, int32_t cap, int32_t *nrounds, int32_t *fused_send,
+                                   int32_t *fused_recv) {
+  if (!ctx || !nrounds) return KRON_ERR_INVALID_ARG;
+  std::vector<int> rounds;
+  kron_status_t st = dist_round_plan(M, N, P, Q, ctx->GM, ctx->GK, &rounds, nullptr);
+  if (st != KRON_OK) return st;
+  *nrounds = (int32_t)rounds.size();
+  const int GK = ctx->GK;
+  std::vector<int64_t> W(N + 1);
+  W[N] = 1;
+  for (int i = 0; i < N; ++i) W[N] *= P[i];
+  for (int f = N; f >= 1; --f) W[f - 1] = W[f] / P[f - 1] * Q[f - 1];
+  const int64_t Ml = M / ctx->GM, nc = std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, Ml));
+  const int64_t rows = (Ml + nc - 1) / nc;
+  int f = N;
+  int64_t prev_rho = 0;
+  for (int j = 0; j < (int)rounds.size(); ++j) {
+    const int k = rounds[j];
+    int64_t C = 1;
+    for (int i = 0; i < k; ++i) C *= P[f - 1 - i];
+    const int64_t wl_in = W[f] / GK, wl_out = W[f - k] / GK;
+    Plan plan;
+    st = make_plan(std::max<int64_t>(rows, 1), k, P + (f - k), Q + (f - k), (int)dtype, &plan, wl_in / C);
+    if (st != KRON_OK) return st;
+    PushArgs pa;
+    pa.B = pa.rho = pa.wd = wl_out / GK;
+    pa.GK = 1;
+    pa.on = 1;
+    InRemap ri;
+    ri.rho = prev_rho;
+    ri.GK = GK;
+    ri.on = 1;
+    if (j < cap) {
+      if (fused_send) fused_send[j] = GK > 1 && GK <= kMaxPush && ctx->fused && ctx->backend != 2 && plan_push_ok(plan, pa);
+      if (fused_recv) fused_recv[j] = GK > 1 && j > 0 && ctx->fused && ctx->backend != 2 && plan_remap_ok(plan, ri);
+    }
+    prev_rho = wl_in / C;
+    f -= k;
+  }
+  return KRON_OK;
+}
+
+}  // extern "C"
+
+namespace kron {
+namespace {
+
+// ---- backend 2: P2P rounds (NEXT-1).  Returns the status; `bufs0` = this rank's scratch.
+kron_status_t dist_p2p(kron_dist_ctx_t *ctx, const std::vector<int> &rounds, std::vector<RoundPlan> &rp, int dtype,
+                       const void *X, const void *const *F, void *Y, RankBufs &b, size_t half, int64_t Ml,
+                       cudaStream_t s) {
+  const int GK = ctx->GK;
+  kron_status_t st = KRON_OK;
+  PeerPtrs heaps{};
+  for (int g = 0; g < GK; ++g) heaps.p[g] = ctx->peer_heap[g];
+  auto barrier = [&]() {
+    const unsigned long long ep = ++ctx->epoch;
+    p2p_barrier_kernel<<<1, 64, 0, s>>>(heaps, reinterpret_cast<unsigned long long *>(ctx->heap), GK, ctx->gK, ep,
+                                        reinterpret_cast<unsigned *>(ctx->heap + kP2PTimeoutOff),
+                                        (long long)20 * 1000 * 1000 * 1000);
+    return cudaGetLastError() == cudaSuccess;
+  };
+  int in_half = -1;  // heap half holding this round's input block (after a push round), else -1
+  for (size_t j = 0; j < rounds.size() && st == KRON_OK; ++j) {
+    const RoundPlan &R = rp[j];
+    const Plan &plan = R.plan[0];
+    const void *const *Fj = F + (R.first - R.k);
+    const bool last = j + 1 == rounds.size();
+    const int64_t B = R.wl_out / GK;  // values per row sent to each peer
+    // this round writes the heap half its input does not occupy
+    const int out_half = in_half >= 0 ? 1 - in_half : (int)ctx->parity;
+    const size_t off = kP2PHeader + (size_t)out_half * half;
+    const void *in = j == 0 ? X : (in_half >= 0 ? (const void *)(ctx->heap + kP2PHeader + (size_t)in_half * half)
+                                                : (const void *)b.cur);
+    ctx->parity = 1u - (unsigned)out_half;
+    PushArgs pa;
+    for (int g = 0; g < GK; ++g) pa.dst[g] = ctx->peer_heap[g] + off;
+    pa.B = B;
+    pa.rho = R.rho;
+    pa.wd = R.wl_out;
+    pa.GK = GK;
+    pa.me = ctx->gK;
+    pa.on = 1;
+    if (!last && ctx->push && GK <= kMaxPush && plan_push_ok(plan, pa)) {
+      // FUSED exchange: the round's last pass stores every value straight into its StoreGPUTile position
+      // in the destination rank's heap half (peer memory over NVLink), so the transfer overlaps the
+      // arithmetic tile by tile.  The passes before it run first — their intermediates may live in this
+      // rank's own heap half, which no peer writes before this rank reaches the barrier — then a barrier
+      // (every peer is done with the half it is about to receive) and the pushing pass, then a barrier
+      // (every value addressed to this rank has landed).
+      const int np = (int)plan.passes.size();
+      if (np > 1 && (st = plan_run(plan, in, Fj, ctx->heap + off, b.ws, s, nullptr, nullptr, 0, np - 1)) != KRON_OK)
+        break;
+      if (!barrier()) { st = KRON_ERR_CUDA; break; }
+      if ((st = plan_run(plan, in, Fj, ctx->heap + off, b.ws, s, &pa, nullptr, np - 1, np)) != KRON_OK) break;
+      if (!barrier()) { st = KRON_ERR_CUDA; break; }
+      in_half = out_half;  // the next round reads its block from this rank's own heap half
+      continue;
+    }
+    // lines 670-674 into this rank's heap half, barrier, then lines 676-690 + 685 as one pull kernel
+    if ((st = plan_run(plan, in, Fj, ctx->heap + off, b.ws, s)) != KRON_OK) break;
+    PeerPtrs outs{};
+    for (int g = 0; g < GK; ++g) outs.p[g] = ctx->peer_heap[g] + off;
+    if (!barrier()) { st = KRON_ERR_CUDA; break; }
+    void *dst = last ? Y : b.cur;
+    if (launch_p2p_pull(dtype, outs, dst, Ml, R.wl_out, R.rho, GK, ctx->gK, s) != 0) st = KRON_ERR_CUDA;
+    in_half = -1;
+  }
+  return st;
+}
+
+}  // namespace
+}  // namespace kron
+
+extern "C" {
+
 kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X_local,
                                const void *const *F, void *Y_local, kron_dtype_t dtype, kron_dist_ctx_t *ctx,
                                void *stream) {
@@ -562,6 +781,8 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
   void *const *Yv = ctx->backend == 1 ? static_cast<void *const *>(Y_local) : &Y_local;
   for (int r = 0; r < nranks; ++r)
     if (!Xv[r] || !Yv[r]) return KRON_ERR_INVALID_ARG;
+  if ((st = nccl_async_status(ctx)) != KRON_OK) return st;  // a collective of an earlier call failed
+  if (ctx->backend == 0 && !ctx->row_comm) return KRON_ERR_NCCL;  // aborted by kron_dist_sync
 
   cudaStream_t s = (cudaStream_t)stream;
   keep_pool_cached();
@@ -572,7 +793,7 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
   for (int i = 0; i < N; ++i) W[N] *= P[i];
   for (int f = N; f >= 1; --f) W[f - 1] = W[f] / P[f - 1] * Q[f - 1];
 
-  // Row-only grid: every rank is an independent single-GPU Kron-Matmul (no communication).
+  // Row-only grid: every rank is an independent single-GPU Kron-Matmul (no communication, P:706-708).
   if (GK == 1) {
     Plan plan;
     st = make_plan(Ml, N, P, Q, (int)dtype, &plan);
@@ -585,35 +806,54 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     return st;
   }
 
+  const bool p2p = ctx->backend == 2;
+  // row chunks (backends 0 / 1): chunk c's all-to-all overlaps chunk c+1's local passes (rows are
+  // independent); P2P rounds run whole
+  const int64_t nc = p2p ? 1 : std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, Ml));
+  const int64_t rows0 = (Ml + nc - 1) / nc, nchunk = (Ml + rows0 - 1) / rows0, rows_last = Ml - (nchunk - 1) * rows0;
+
   // local plans per round (identical on every rank: shape-only)
-  struct RoundPlan {
-    Plan plan;
-    int first;
-    int64_t wl_in, wl_out, rho;
-  };
   std::vector<RoundPlan> rp(rounds.size());
   int64_t max_w = 0;
   size_t ws_max = 0;
+  bool need_cur = false, need_out = false;
   {
     int f = N;
     for (size_t j = 0; j < rounds.size(); ++j) {
-      const int k = rounds[j];
+      RoundPlan &R = rp[j];
+      R.k = rounds[j];
       int64_t C = 1;
-      for (int i = 0; i < k; ++i) C *= P[f - 1 - i];
-      rp[j].first = f;
-      rp[j].wl_in = W[f] / GK;
-      rp[j].wl_out = W[f - k] / GK;
-      rp[j].rho = rp[j].wl_in / C;
+      for (int i = 0; i < R.k; ++i) C *= P[f - 1 - i];
+      R.first = f;
+      R.wl_in = W[f] / GK;
+      R.wl_out = W[f - R.k] / GK;
+      R.rho = R.wl_in / C;
       // factors f-k+1 .. f (most significant first) on the local block with lead = wl_in / C
-      st = make_plan(Ml, k, P + (f - k), Q + (f - k), (int)dtype, &rp[j].plan, rp[j].wl_in / C);
-      if (st != KRON_OK) return st;
-      max_w = std::max(max_w, std::max(rp[j].wl_in, rp[j].wl_out));
-      ws_max = std::max(ws_max, plan_ws_bytes(rp[j].plan));
-      f -= k;
+      for (int v = 0; v < 2; ++v) {
+        st = make_plan(v == 0 ? rows0 : rows_last, R.k, P + (f - R.k), Q + (f - R.k), (int)dtype, &R.plan[v],
+                       R.wl_in / C);
+        if (st != KRON_OK) return st;
+        ws_max = std::max(ws_max, plan_ws_bytes(R.plan[v]));
+      }
+      if (!p2p && ctx->fused) {
+        PushArgs pa;
+        pa.B = pa.rho = pa.wd = R.wl_out / GK;
+        pa.GK = 1;
+        pa.on = 1;
+        InRemap ri;
+        ri.rho = j > 0 ? rp[j - 1].rho : 0;
+        ri.GK = GK;
+        ri.on = 1;
+        R.fpush = GK <= kMaxPush && plan_push_ok(R.plan[0], pa) && plan_push_ok(R.plan[1], pa);
+        R.fremap = j > 0 && plan_remap_ok(R.plan[0], ri) && plan_remap_ok(R.plan[1], ri);
+      }
+      need_out |= !R.fpush;
+      need_cur |= j > 0 && !R.fremap;
+      max_w = std::max(max_w, std::max(R.wl_in, R.wl_out));
+      f -= R.k;
     }
   }
   const size_t buf_bytes = (size_t)Ml * max_w * es;
-  const bool p2p = ctx->backend == 2;
   size_t half = 0;
   if (p2p) {
     // the round outputs live in the symmetric heap (two halves); see kron_dist_p2p_heap_bytes
@@ -623,13 +863,15 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     if (!ctx->connected) return KRON_ERR_INVALID_ARG;
     if (need > ctx->heap_bytes) return KRON_ERR_NO_MEMORY;
     half = need / 2;
+    need_cur = true;
+    need_out = false;
   }
   std::vector<RankBufs> bufs(nranks);
   bool oom = false;
   for (int r = 0; r < nranks; ++r) {
-    oom |= cudaMallocAsync(&bufs[r].cur, buf_bytes, s) != cudaSuccess;
+    if (need_cur) oom |= cudaMallocAsync(&bufs[r].cur, buf_bytes, s) != cudaSuccess;
     if (!p2p) {
-      oom |= cudaMallocAsync(&bufs[r].out, buf_bytes, s) != cudaSuccess;
+      if (need_out) oom |= cudaMallocAsync(&bufs[r].out, buf_bytes, s) != cudaSuccess;
       oom |= cudaMallocAsync(&bufs[r].send, buf_bytes, s) != cudaSuccess;
       oom |= cudaMallocAsync(&bufs[r].recv, buf_bytes, s) != cudaSuccess;
     }
@@ -645,91 +887,121 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
     free_all();
     return KRON_ERR_NO_MEMORY;
   }
+  if (p2p) {
+    st = dist_p2p(ctx, rounds, rp, (int)dtype, Xv[0], F, Yv[0], bufs[0], half, Ml, s);
+    free_all();
+    return st;
+  }
 
-  int p2p_in_half = -1;  // P2P: heap half holding this round's input block (after a push round), else -1
+  // ---- backends 0 (NCCL) and 1 (virtual): per round and row chunk
+  //   lines 670-674: local passes; the last one writes the destination-major send block send[d][rows][B]
+  //                  (fused pack) or the plain block + a pack kernel
+  //   lines 676-692: one all-to-all within the row group (NCCL on the context's comm stream, overlapping the
+  //                  next chunk's passes; virtual: device copies)
+  //   line 685:      StoreGPUTile — done by the next round's first pass through the remapped tensor map
+  //                  (fused), else by a kernel into the next round's block; after the last round into Y_local
+  const bool nccl_be = ctx->backend == 0;
+  cudaStream_t sc = s;
+  cudaEvent_t *ev = nullptr;
+  if (nccl_be) {
+    if (!ctx->comm && cudaStreamCreateWithFlags(&ctx->comm, cudaStreamNonBlocking) != cudaSuccess) st = KRON_ERR_CUDA;
+    while (st == KRON_OK && ctx->ev.size() < (size_t)(1 + 2 * nchunk)) {
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) st = KRON_ERR_CUDA;
+      else ctx->ev.push_back(e);
+    }
+    if (st != KRON_OK) {
+      free_all();
+      return st;
+    }
+    sc = ctx->comm;
+    ev = ctx->ev.data();
+    // the comm stream starts after the caller's prior work and the stream-ordered allocations
+    if (cudaEventRecord(ev[0], s) != cudaSuccess || cudaStreamWaitEvent(sc, ev[0], 0) != cudaSuccess) st = KRON_ERR_CUDA;
+  }
+  const int64_t Kl = W[N] / GK, Ll = W[0] / GK;
   for (size_t j = 0; j < rounds.size() && st == KRON_OK; ++j) {
     const RoundPlan &R = rp[j];
-    const int k = rounds[j];
-    const void *const *Fj = F + (R.first - k);
-    const bool last = j + 1 == rounds.size();
-    const int64_t B = R.wl_out / GK;       // values per row sent to each peer
-    const size_t blk = (size_t)Ml * B;     // values per peer
-    if (p2p) {
-      PeerPtrs heaps{};
-      for (int g = 0; g < GK; ++g) heaps.p[g] = ctx->peer_heap[g];
-      auto barrier = [&]() {
-        const unsigned long long ep = ++ctx->epoch;
-        p2p_barrier_kernel<<<1, 64, 0, s>>>(heaps, reinterpret_cast<unsigned long long *>(ctx->heap), GK, ctx->gK,
-                                            ep, reinterpret_cast<unsigned *>(ctx->heap + kP2PTimeoutOff),
-                                            (long long)20 * 1000 * 1000 * 1000);
-        return cudaGetLastError() == cudaSuccess;
-      };
-      // this round writes the heap half its input does not occupy
-      const int out_half = p2p_in_half >= 0 ? 1 - p2p_in_half : (int)ctx->parity;
-      const size_t off = kP2PHeader + (size_t)out_half * half;
-      const void *in = j == 0 ? Xv[0] : (p2p_in_half >= 0 ? (const void *)(ctx->heap + kP2PHeader +
-                                                                           (size_t)p2p_in_half * half)
-                                                          : (const void *)bufs[0].cur);
-      ctx->parity = 1u - (unsigned)out_half;
-      if (!last && GK <= kMaxPush && plan_push_ok(R.plan) && !getenv("KRON_P2P_NO_PUSH")) {
-        // FUSED exchange: the round's last pass stores every value straight into its StoreGPUTile position
-        // in the destination rank's heap half (peer memory over NVLink), so the transfer overlaps the
-        // arithmetic tile by tile.  Barrier before (every rank finished reading that half and pulling from
-        // the previous round) and after (every value addressed to this rank has landed).
-        if (!barrier()) { st = KRON_ERR_CUDA; break; }
-        PushArgs pa;
-        for (int g = 0; g < GK; ++g) pa.dst[g] = ctx->peer_heap[g] + off;
-        pa.B = B;
-        pa.rho = R.rho;
-        pa.wd = R.wl_out;
-        pa.GK = GK;
-        pa.me = ctx->gK;
-        pa.on = 1;
-        st = plan_run(R.plan, in, Fj, ctx->heap + off, bufs[0].ws, stream, &pa);
-        if (st != KRON_OK) break;
-        if (!barrier()) { st = KRON_ERR_CUDA; break; }
-        p2p_in_half = out_half;  // the next round reads its block from this rank's own heap half
-        continue;
-      }
-      // lines 670-674 into this rank's heap half, barrier, then lines 676-690 + 685 as one pull kernel
-      st = plan_run(R.plan, in, Fj, ctx->heap + off, bufs[0].ws, stream);
-      if (st != KRON_OK) break;
-      PeerPtrs outs{};
-      for (int g = 0; g < GK; ++g) outs.p[g] = ctx->peer_heap[g] + off;
-      if (!barrier()) { st = KRON_ERR_CUDA; break; }
-      void *dst = last ? Yv[0] : bufs[0].cur;
-      if (launch_p2p_pull((int)dtype, outs, dst, Ml, R.wl_out, R.rho, GK, ctx->gK, s) != 0) st = KRON_ERR_CUDA;
-      p2p_in_half = -1;
-      continue;
-    }
-    // lines 670-674: local sliced multiplies; then pack the destination-major send buffer
-    for (int r = 0; r < nranks && st == KRON_OK; ++r) {
-      const void *in = j == 0 ? Xv[r] : bufs[r].cur;
-      st = plan_run(R.plan, in, Fj, bufs[r].out, bufs[r].ws, stream);
-      if (st == KRON_OK && launch_pack((int)dtype, bufs[r].out, bufs[r].send, Ml, R.wl_out, B, s) != 0)
-        st = KRON_ERR_CUDA;
-    }
-    if (st != KRON_OK) break;
-    // lines 676-692: all-to-all inside the row group
-    if (ctx->backend == 0) {
-      st = exchange_nccl(ctx, (int)dtype, bufs[0].send, bufs[0].recv, blk, s);
-    } else {
-      for (int gm = 0; gm < GM && st == KRON_OK; ++gm)
-        for (int src = 0; src < GK; ++src)
-          for (int dst = 0; dst < GK; ++dst) {
-            const int rs = gm * GK + src, rd = gm * GK + dst;
-            if (cudaMemcpyAsync(static_cast<char *>(bufs[rd].recv) + (size_t)src * blk * es,
-                                static_cast<const char *>(bufs[rs].send) + (size_t)dst * blk * es, blk * es,
-                                cudaMemcpyDeviceToDevice, s) != cudaSuccess)
-              st = KRON_ERR_CUDA;
+    const void *const *Fj = F + (R.first - R.k);
+    const int64_t B = R.wl_out / GK;
+    for (int64_t c = 0; c < nchunk && st == KRON_OK; ++c) {
+      const int64_t r0 = c * rows0, rows = c + 1 < nchunk ? rows0 : rows_last;
+      const Plan &plan = R.plan[c + 1 < nchunk ? 0 : 1];
+      const size_t blk = (size_t)rows * B;  // values per peer
+      if (j > 0 && nccl_be && cudaStreamWaitEvent(s, ev[2 + 2 * c], 0) != cudaSuccess) st = KRON_ERR_CUDA;
+      for (int r = 0; r < nranks && st == KRON_OK; ++r) {
+        RankBufs &b = bufs[r];
+        // this chunk's input: X, the previous round's receive block (remapped view) or its StoreGPUTile copy
+        const void *in;
+        InRemap ri;
+        if (j == 0) {
+          in = at(Xv[r], r0 * Kl, es);
+        } else if (R.fremap) {
+          in = at(b.recv, r0 * R.wl_in, es);
+          ri.rho = rp[j - 1].rho;
+          ri.GK = GK;
+          ri.on = 1;
+        } else {
+          void *cur = at(b.cur, r0 * R.wl_in, es);
+          if (launch_store_gpu_tile((int)dtype, at(b.recv, r0 * R.wl_in, es), cur, rows, R.wl_in, rp[j - 1].rho, GK,
+                                    s) != 0) {
+            st = KRON_ERR_CUDA;
+            break;
           }
+          in = cur;
+        }
+        char *send = at(b.send, r0 * R.wl_out, es);
+        if (R.fpush) {
+          PushArgs pa;
+          for (int d = 0; d < GK; ++d) pa.dst[d] = send + (size_t)d * blk * es;
+          pa.B = pa.rho = pa.wd = B;
+          pa.GK = 1;
+          pa.me = 0;
+          pa.on = 1;
+          // intermediates (if any) ping-pong through ws and this chunk's receive block region is not touched;
+          // Y of the plan (never written by a pushing last pass) is the send block itself
+          st = plan_run(plan, in, Fj, send, b.ws, s, &pa, R.fremap ? &ri : nullptr);
+        } else {
+          void *outb = at(b.out, r0 * R.wl_out, es);
+          st = plan_run(plan, in, Fj, outb, b.ws, s, nullptr, R.fremap ? &ri : nullptr);
+          if (st == KRON_OK && launch_pack((int)dtype, outb, send, rows, R.wl_out, B, s) != 0) st = KRON_ERR_CUDA;
+        }
+      }
+      if (st != KRON_OK) break;
+      if (nccl_be) {
+        if (cudaEventRecord(ev[1 + 2 * c], s) != cudaSuccess || cudaStreamWaitEvent(sc, ev[1 + 2 * c], 0) != cudaSuccess) {
+          st = KRON_ERR_CUDA;
+          break;
+        }
+        st = exchange_nccl(ctx, (int)dtype, at(bufs[0].send, r0 * R.wl_out, es), at(bufs[0].recv, r0 * R.wl_out, es),
+                           blk, sc);
+        if (st == KRON_OK && cudaEventRecord(ev[2 + 2 * c], sc) != cudaSuccess) st = KRON_ERR_CUDA;
+      } else {
+        for (int gm = 0; gm < GM && st == KRON_OK; ++gm)
+          for (int src = 0; src < GK; ++src)
+            for (int dst = 0; dst < GK; ++dst) {
+              const int rs = gm * GK + src, rd = gm * GK + dst;
+              if (cudaMemcpyAsync(at(bufs[rd].recv, r0 * R.wl_out + (int64_t)src * (int64_t)blk, es),
+                                  at(bufs[rs].send, r0 * R.wl_out + (int64_t)dst * (int64_t)blk, es), blk * es,
+                                  cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+                st = KRON_ERR_CUDA;
+            }
+      }
     }
-    if (st != KRON_OK) break;
-    // line 685: StoreGPUTile into the next round's local block (or Y_local after the last round)
-    for (int r = 0; r < nranks && st == KRON_OK; ++r) {
-      void *dst = last ? Yv[r] : bufs[r].cur;
-      if (launch_store_gpu_tile((int)dtype, bufs[r].recv, dst, Ml, R.wl_out, R.rho, GK, s) != 0) st = KRON_ERR_CUDA;
-    }
+  }
+  // line 685 after the last round: StoreGPUTile into Y_local (natural column block gK*L/GK ...)
+  const RoundPlan &RL = rp.back();
+  for (int64_t c = 0; c < nchunk && st == KRON_OK; ++c) {
+    const int64_t r0 = c * rows0, rows = c + 1 < nchunk ? rows0 : rows_last;
+    if (nccl_be && cudaStreamWaitEvent(s, ev[2 + 2 * c], 0) != cudaSuccess) st = KRON_ERR_CUDA;
+    for (int r = 0; r < nranks && st == KRON_OK; ++r)
+      if (launch_store_gpu_tile((int)dtype, at(bufs[r].recv, r0 * RL.wl_out, es), at(Yv[r], r0 * Ll, es), rows,
+                                RL.wl_out, RL.rho, GK, s) != 0)
+        st = KRON_ERR_CUDA;
+  }
+  if (st != KRON_OK && nccl_be) {
+    // keep the buffers alive until whatever was enqueued on the comm stream has finished
+    for (int64_t c = 0; c < nchunk; ++c) cudaStreamWaitEvent(s, ev[2 + 2 * c], 0);
   }
   free_all();
   return st;

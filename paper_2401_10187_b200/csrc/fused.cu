@@ -45,13 +45,6 @@ struct FusedArgs {
   int nslices;    // tileM * Sl
   int C;          // chunk = P^nf
   int nout;       // output buffers (warp-chain kernel): 2 = double-buffered TMA-store source
-  // L2-fused pair mode (factor-pipeline kernel): CTAs with odd blockIdx run the second pass of the
-  // pair, consuming rows of the first pass's output from a ring of NR rows that stays in L2
-  int pair;
-  const void *F2[kMaxFused];  // second-pass factors
-  int *produced;              // [M] tiles of row r written to the ring by the first pass
-  int *consumed;              // [M] tiles of row r loaded from the ring by the second pass
-  int NR;                     // ring rows
   void *Y;        // output matrix (kernels that store from registers)
   int64_t WC;     // W / C  (output column stride of a composite column u)
   int64_t Wout;   // output row width
@@ -63,8 +56,25 @@ struct FusedArgs {
   uint32_t tile_bytes;
   uint32_t stage_bytes;
   int stages;
-  PushArgs push;  // v9: distributed P2P push of the pass's output (push.on)
+  PushArgs push;  // v9 / v6: the pass's output goes to per-destination buffers (distributed round, push.on)
+  // distributed round input read in place from an all-to-all receive buffer (InRemap): local line l ->
+  // run = l / rmp_rl, (e, src) = (run / rmp_GK, run % rmp_GK); 5-D map coordinates {0, l % rl, src, e, row}
+  int rmp_rl;  // 0: plain 3-D [row][line][32] input map
+  int rmp_GK;
 };
+
+// One input box of a fused pass (rows x 128-byte lines from `line`): the plain 3-D map, or the 5-D
+// StoreGPUTile view of a receive buffer (Alg 2 line 685 done by the TMA engine's address generation).
+__device__ __forceinline__ void load_in(const FusedArgs &a, void *dst, const CUtensorMap *m, uint64_t *bar, int line,
+                                        int row) {
+  if (a.rmp_rl) {
+    const int run = line / a.rmp_rl, tl = line - run * a.rmp_rl;
+    const int e = run / a.rmp_GK, src = run - e * a.rmp_GK;
+    tma_load_5d(dst, m, bar, 0, tl, src, e, row);
+  } else {
+    tma_load_3d(dst, m, bar, 0, line, row);
+  }
+}
 
 namespace {
 
@@ -253,7 +263,7 @@ __global__ void __launch_bounds__(NT) kron_fused_kernel(const __grid_constant__ 
     mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb * a.tileM);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], line0 + b * a.box_lines, rb * a.tileM);
   };
 
   if (tid == 0)
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(NT, MINB) kron_fused_warp_kernel(const __grid_
     mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb * a.tileM);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], line0 + b * a.box_lines, rb * a.tileM);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
@@ -575,33 +585,15 @@ struct VecIO<double, 2> {
   }
 };
 
-template <typename T, int P, int NWG, int VS, int G, bool PAIR>
+template <typename T, int P, int NWG, int VS, int G>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
-                                           int wg, int lane, int tid, int role, int cta, int ncta);
+                                           int wg, int lane, int tid);
 
-__device__ __forceinline__ int ld_acquire(const int *p) {
-  int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
-
-// spin (with back-off) until *p >= target
-__device__ __forceinline__ void wait_counter(const int *p, int target) {
-  if (ld_acquire(p) >= target) return;
-  unsigned ns = 64;
-  while (ld_acquire(p) < target) {
-    __nanosleep(ns);
-    if (ns < 1024) ns <<= 1;
-  }
-}
-
-template <typename T, int P, int NWG, int VS, bool PAIR>
-__global__ void __launch_bounds__(32 * (1 + NWG * 3), PAIR ? 2 : 1)
+template <typename T, int P, int NWG, int VS>
+__global__ void __launch_bounds__(32 * (1 + NWG * 3), 1)
     kron_fused_pipe_kernel(const __grid_constant__ CUtensorMap tm_in, const __grid_constant__ CUtensorMap tm_out,
-                           const FusedArgs a, const __grid_constant__ CUtensorMap tm_in2,
-                           const __grid_constant__ CUtensorMap tm_out2) {
+                           const FusedArgs a) {
   constexpr int ES = sizeof(T);               // VS: consecutive slices (middle) / chunks (last) per thread
   constexpr int LINE = 128 / ES;
   constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
@@ -619,11 +611,7 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), PAIR ? 2 : 1)
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
   const int nf = a.nf;
 
-  const int role = PAIR ? (int)(blockIdx.x & 1u) : 0;
-  const int cta = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int ncta = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
-  const CUtensorMap *tin = (PAIR && role) ? &tm_in2 : &tm_in;
-  const CUtensorMap *tout = (PAIR && role) ? &tm_out2 : &tm_out;
+  const CUtensorMap *tin = &tm_in, *tout = &tm_out;
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
       mbar_init(&full[s], 1);
@@ -641,24 +629,15 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), PAIR ? 2 : 1)
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int64_t tile = cta, it = 0; tile < a.ntiles; tile += ncta, ++it) {
+      for (int64_t tile = blockIdx.x, it = 0; tile < a.ntiles; tile += gridDim.x, ++it) {
         if (it >= a.stages) mbar_wait(&empty[st], ph ^ 1u);
         const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
-        int lrow = rb * a.tileM;
-        if constexpr (PAIR) {
-          if (role == 0) {
-            if (rb >= a.NR) wait_counter(&a.consumed[rb - a.NR], a.tiles_k);  // ring slot is free
-          } else {
-            wait_counter(&a.produced[rb], a.tiles_k);  // the whole row of the first pass is in the ring
-            fence_proxy_async_global();
-            lrow = rb % a.NR;
-          }
-        }
+        const int lrow = rb * a.tileM;
         unsigned char *dst = base + (size_t)st * a.stage_bytes;
         mbar_arrive_expect_tx(&full[st], a.tile_bytes);
         const int line0 = cb * (a.tileK / LINE);
         for (int b = 0; b < a.nbox; ++b)
-          tma_load_3d(dst + (size_t)b * a.box_lines * 128, tin, &full[st], 0, line0 + b * a.box_lines, lrow);
+          load_in(a, dst + (size_t)b * a.box_lines * 128, tin, &full[st], line0 + b * a.box_lines, lrow);
         if (++st == a.stages) {
           st = 0;
           ph ^= 1u;
@@ -671,15 +650,16 @@ __global__ void __launch_bounds__(32 * (1 + NWG * 3), PAIR ? 2 : 1)
   if (g >= nf) return;
   // one code path per group index so that the factor pointer (kernel parameter) and hence every
   // factor value is provably warp-uniform: the compiler keeps F in uniform registers
-  if (g == 0) pipe_group<T, P, NWG, VS, 0, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
-  else if (g == 1) pipe_group<T, P, NWG, VS, 1, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
-  else pipe_group<T, P, NWG, VS, 2, PAIR>(a, tout, base, obase, full, empty, done, wg, lane, tid, role, cta, ncta);
+  if (g == 0) pipe_group<T, P, NWG, VS, 0>(a, tout, base, obase, full, empty, done, wg, lane, tid);
+  else if (g == 1) pipe_group<T, P, NWG, VS, 1>(a, tout, base, obase, full, empty, done, wg, lane, tid);
+  else pipe_group<T, P, NWG, VS, 2>(a, tout, base, obase, full, empty, done, wg, lane, tid);
 }
 
-template <typename T, int P, int NWG, int VS, int G, bool PAIR>
+template <typename T, int P, int NWG, int VS, int G>
 __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap *tm_out, unsigned char *base,
                                            unsigned char *obase, uint64_t *full, uint64_t *empty, uint64_t *done,
-                                           int wg, int lane, int tid, int role, int cta, int ncta) {
+                                           int wg, int lane, int tid) {
+  const int cta = (int)blockIdx.x, ncta = (int)gridDim.x;
   constexpr int ES = sizeof(T);
   constexpr int NV = P * ES / 16 > 0 ? P * ES / 16 : 1;  // 16-byte loads per slice
   constexpr int EPV = 16 / ES > P ? P : 16 / ES;
@@ -687,7 +667,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   const int g = G, nf = a.nf;
   // this group's factor F_{first-g} lives in (uniform) registers for the whole kernel
   RegFactor<T, P> Fr;
-  Fr.load(reinterpret_cast<const T *>((PAIR && role) ? a.F2[G] : a.F[G]));
+  Fr.load(reinterpret_cast<const T *>(a.F[G]));
   const uint32_t C = (uint32_t)a.C, CP = C / P, R = (uint32_t)a.R;
   const uint32_t tile_elems = (uint32_t)a.tileM * (uint32_t)a.tileK;
   const bool gx_on = C * ES >= 128;  // the granule XOR must be constant over each 128-byte line
@@ -702,11 +682,6 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
     uint32_t ph = 0;
     for (int64_t tile = cta; tile < a.ntiles; tile += ncta) {
       mbar_wait(g == 0 ? &full[st] : &done[(g - 1) * a.stages + st], ph);
-      if (PAIR && role == 1 && g == 0 && wg == 0 && lane == 0) {
-        // the tile has left the ring (TMA bytes landed): count it for the first pass's back-pressure
-        __threadfence();
-        atomicAdd(&a.consumed[tile / a.tiles_k], 1);
-      }
       unsigned char *buf = base + (size_t)st * a.stage_bytes;
 #pragma unroll 1
       for (uint32_t grp = (uint32_t)wg; grp < nreg; grp += NWG) {
@@ -775,8 +750,6 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
   }
   int st = 0;
   uint32_t ph = 0;
-  const bool signal = PAIR && role == 0;  // first pass of a pair: publish finished ring rows
-  int64_t prev_row = -1;
   for (int64_t tile = cta, it = 0; tile < a.ntiles; tile += ncta, ++it) {
     mbar_wait(nf == 1 ? &full[st] : &done[(nf - 2) * a.stages + st], ph);
     named_bar_sync(1, LT);  // the store that last read this output buffer has finished reading it
@@ -822,33 +795,16 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
     if (lt == 0) {
       mbar_arrive(&empty[st]);  // every group is done with this stage
       const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
-      tma_store_4d(tm_out, obuf, cb * a.R, 0, 0, signal ? rb % a.NR : rb * a.tileM);
+      tma_store_4d(tm_out, obuf, cb * a.R, 0, 0, rb * a.tileM);
       bulk_commit();
-      if (signal) {
-        bulk_wait<1>();  // the previous tile's store has completed: publish its row
-        if (prev_row >= 0) {
-          fence_proxy_async_global();
-          __threadfence();
-          atomicAdd(&a.produced[prev_row], 1);
-        }
-        prev_row = rb;
-      } else {
-        bulk_wait_read<1>();
-      }
+      bulk_wait_read<1>();
     }
     if (++st == a.stages) {
       st = 0;
       ph ^= 1u;
     }
   }
-  if (lt == 0) {
-    bulk_wait<0>();
-    if (signal && prev_row >= 0) {
-      fence_proxy_async_global();
-      __threadfence();
-      atomicAdd(&a.produced[prev_row], 1);
-    }
-  }
+  if (lt == 0) bulk_wait<0>();
 }
 
 // ------------------------------------------------------------------ two-factor GEMM chunks (v4)
@@ -902,7 +858,7 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
     mbar_arrive_expect_tx(&bars[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], 0, line0 + b * a.box_lines, rb);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &bars[st], line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
@@ -1187,7 +1143,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
     mbar_arrive_expect_tx(&full[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
@@ -1463,7 +1419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
     mbar_arrive_expect_tx(&full[st], TB);
     const int line0 = (gj * 8 + (int)rank * 4) * (4096 / 32);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < S; ++it) issue_load(it);
@@ -1751,7 +1707,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
     mbar_arrive_expect_tx(&full[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
@@ -2099,7 +2055,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_tf32x3_kernel(
     mbar_arrive_expect_tx(&full[st], a.tile_bytes);
     const int line0 = cb * (a.tileK / LINE);
     for (int b = 0; b < a.nbox; ++b)
-      tma_load_3d(dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], 0, line0 + b * a.box_lines, rb);
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], line0 + b * a.box_lines, rb);
   };
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
@@ -2269,8 +2225,9 @@ const FusedInstance kInstances[] = {
     // v4: two-factor chunk GEMMs (tile = 256 * RS * P elements = 8192)
     {KRON_F32, 16, 256, 2, 3, 0}, {KRON_F32, 32, 256, 1, 3, 0},
     {KRON_F64, 16, 256, 1, 3, 0}, {KRON_F64, 32, 256, 1, 3, 0},
-    // L2-fused pair of factor pipelines (two passes in one cooperative launch): id 29
-    {KRON_F32, 8, 64, 8, 4, 2},
+    // id 29: retired (round 1's experimental L2-fused pair of factor pipelines, measured slower than two
+    // passes on config B; removed in round 2).  Kept as a never-selected slot so the ids below stay put.
+    {KRON_F32, 8, 64, 8, -1, 2},
     // v5: fp64 two-factor chunks on DMMA (P = 32, tile = 256 * RS * P = 8 chunks = 64-byte output runs;
     //     4-chunk tiles (32-byte runs) measured 9.42 ms on C64 vs 8.93 ms): id 30
     {KRON_F64, 32, 256, 1, 5, 0},
@@ -2290,7 +2247,6 @@ const FusedInstance kInstances[] = {
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
 using KernelFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs);
-using KernelPFn = void (*)(const CUtensorMap, const CUtensorMap, const FusedArgs, const CUtensorMap, const CUtensorMap);
 using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
@@ -2307,14 +2263,13 @@ Kernel4Fn instance_kernel4(int i) {
   return nullptr;
 }
 
-KernelPFn instance_pipe(int i) {
+KernelFn instance_pipe(int i) {
   switch (i) {
-    case 0: return kron_fused_pipe_kernel<float, 2, 4, 4, false>;
-    case 1: return kron_fused_pipe_kernel<float, 4, 4, 4, false>;
-    case 2: return kron_fused_pipe_kernel<float, 8, 4, 2, false>;
-    case 3: return kron_fused_pipe_kernel<double, 2, 4, 2, false>;
-    case 4: return kron_fused_pipe_kernel<double, 4, 4, 2, false>;
-    case 29: return kron_fused_pipe_kernel<float, 8, 2, 2, true>;
+    case 0: return kron_fused_pipe_kernel<float, 2, 4, 4>;
+    case 1: return kron_fused_pipe_kernel<float, 4, 4, 4>;
+    case 2: return kron_fused_pipe_kernel<float, 8, 4, 2>;
+    case 3: return kron_fused_pipe_kernel<double, 2, 4, 2>;
+    case 4: return kron_fused_pipe_kernel<double, 4, 4, 2>;
   }
   return nullptr;
 }
@@ -2386,22 +2341,38 @@ bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const u
 
 // Host-side launch bookkeeping is cached per (kernel, block, smem): cudaFuncSetAttribute and the
 // occupancy query cost microseconds, which dominate small problems (Table 4 sizes).
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<const void *, int>, size_t> g_attr;  // dynamic-smem limit set per (kernel, device)
+
+// caller holds g_attr_mu; the attribute only ever grows, so launches with any smaller smem stay valid
+int set_smem_attr_locked(const void *fn, size_t smem, int dev) {
+  size_t &cur = g_attr[std::make_pair(fn, dev)];
+  if (smem > cur) {
+    const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return (int)e;
+    cur = smem;
+  }
+  return 0;
+}
+}  // namespace
+
+int set_smem_attr(const void *fn, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  return set_smem_attr_locked(fn, smem, dev);
+}
+
 int kernel_slots(const void *fn, int threads, size_t smem) {
-  static std::mutex mu;
   static std::map<std::tuple<const void *, int, size_t, int>, int> cache;
-  static std::map<std::pair<const void *, int>, size_t> attr;  // dynamic-smem limit set per (kernel, device)
   int dev = 0;
   cudaGetDevice(&dev);
   const auto key = std::make_tuple(fn, threads, smem, dev);
-  std::lock_guard<std::mutex> lk(mu);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
   auto it = cache.find(key);
   if (it != cache.end()) return it->second;
-  // the attribute only ever grows, so launches with any smaller smem stay valid
-  size_t &cur = attr[std::make_pair(fn, dev)];
-  if (smem > cur) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) return -1;
-    cur = smem;
-  }
+  if (set_smem_attr_locked(fn, smem, dev) != 0) return -1;
   int per_sm = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess) return -1;
   int sms = 148;
@@ -2419,8 +2390,14 @@ int fused_find(int dtype, int P, int warp) {
   return -1;
 }
 
+int fused_box_lines(const PassPlan &pp, int dtype) {
+  const int line = dtype == KRON_F32 ? 32 : 16;
+  const int lines = (int)(pp.tileK / line);
+  return lines > 256 ? 256 : lines;
+}
+
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *aux, void *stream, const PushArgs *push) {
+                 void *stream, const PushArgs *push, const InRemap *rin) {
   const FusedInstance &inst = kInstances[pp.variant];
   const int es = dtype == KRON_F32 ? 4 : 8;
   const int line = 128 / es;
@@ -2439,12 +2416,13 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   const int64_t tiles_m = (M + pp.tileM - 1) / pp.tileM;
   a.ntiles = tiles_m * a.tiles_k;
   const int lines = (int)(pp.tileK / line);
-  a.box_lines = lines > 256 ? 256 : lines;
+  a.box_lines = fused_box_lines(pp, dtype);
   a.nbox = lines / a.box_lines;
   a.tile_bytes = (uint32_t)(pp.tileM * pp.tileK * es);
   a.stage_bytes = (a.tile_bytes + 1023u) & ~1023u;
   a.stages = pp.stages;
 
+  if (rin && rin->on && inst.warp == 7) return (int)cudaErrorInvalidValue;
   if (inst.warp == 7) {
     // 5-D map over X[m][g][s][p/16][p%16]; box = one p-half of one chunk ([64][2][16] = 16 KB)
     CUtensorMap t5;
@@ -2466,7 +2444,28 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     return (int)cudaGetLastError();
   }
   CUtensorMap tin, tout;
-  {
+  if (rin && rin->on) {
+    // receive buffer recv[src][m][e*rho + t] (B = W/GK values per row and source) seen in local-column order
+    // (e*GK + src)*rho + t: dims {line, rho/line, GK, B/rho, M}; a box covers whole runs or lies in one
+    const int64_t rl = rin->rho / line, GK = rin->GK, B = W / GK, bl = a.box_lines;
+    if (rin->rho % line || W % (rin->rho * GK)) return (int)cudaErrorInvalidValue;
+    uint64_t dims[5] = {(uint64_t)line, (uint64_t)rl, (uint64_t)GK, (uint64_t)(B / rin->rho), (uint64_t)M};
+    uint64_t strides[4] = {128, (uint64_t)(M * B * es), (uint64_t)(rin->rho * es), (uint64_t)(B * es)};
+    uint32_t box[5] = {(uint32_t)line, 1, 1, 1, (uint32_t)pp.tileM};
+    if (bl <= rl) {
+      if (rl % bl) return (int)cudaErrorInvalidValue;
+      box[1] = (uint32_t)bl;
+    } else {
+      const int64_t nr = bl / rl;
+      if (bl % rl || (nr <= GK ? GK % nr : nr % GK)) return (int)cudaErrorInvalidValue;
+      box[1] = (uint32_t)rl;
+      box[2] = (uint32_t)(nr <= GK ? nr : GK);
+      box[3] = (uint32_t)(nr <= GK ? 1 : nr / GK);
+    }
+    if (!encode_tmap(&tin, dtype, 5, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
+    a.rmp_rl = (int)rl;
+    a.rmp_GK = (int)GK;
+  } else {
     uint64_t dims[3] = {(uint64_t)line, (uint64_t)(W / line), (uint64_t)M};
     uint64_t strides[2] = {128, (uint64_t)W * es};
     uint32_t box[3] = {(uint32_t)line, (uint32_t)a.box_lines, (uint32_t)pp.tileM};
@@ -2480,26 +2479,6 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     if (!encode_tmap(&tout, dtype, 4, out, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
   }
 
-  CUtensorMap tin2 = tin, tout2 = tout;
-  if (inst.warp == 4) {
-    // L2-fused pair: pass 1 writes a ring of NR rows (aux), pass 2 reads it; per-row counters follow
-    a.pair = 1;
-    a.NR = pp.ring_rows;
-    for (int i = 0; i < pp.nf; ++i) a.F2[i] = Fgroup[pp.nf + i];
-    a.produced = reinterpret_cast<int *>(static_cast<char *>(aux) + (size_t)pp.ring_rows * W * es);
-    a.consumed = a.produced + M;
-    const int64_t qlo = pp.Qc > 256 ? 256 : pp.Qc, qhi = pp.Qc / qlo;
-    uint64_t d1[4] = {(uint64_t)WC, (uint64_t)qlo, (uint64_t)qhi, (uint64_t)pp.ring_rows};
-    uint64_t s1[3] = {(uint64_t)WC * es, (uint64_t)(WC * qlo * es), (uint64_t)W * es};
-    uint32_t b1[4] = {(uint32_t)pp.R, (uint32_t)qlo, (uint32_t)qhi, 1};
-    if (!encode_tmap(&tout, dtype, 4, aux, d1, s1, b1, false)) return (int)cudaErrorInvalidValue;
-    uint64_t d2[3] = {(uint64_t)line, (uint64_t)(W / line), (uint64_t)pp.ring_rows};
-    uint64_t s2[2] = {128, (uint64_t)W * es};
-    uint32_t b2[3] = {(uint32_t)line, (uint32_t)a.box_lines, 1};
-    if (!encode_tmap(&tin2, dtype, 3, aux, d2, s2, b2, true)) return (int)cudaErrorInvalidValue;
-    if (cudaMemsetAsync(a.produced, 0, 2 * (size_t)M * sizeof(int), (cudaStream_t)stream) != cudaSuccess)
-      return (int)cudaGetLastError();
-  }
   a.nout = pp.nout;
   a.Y = out;
   a.WC = WC;
@@ -2516,7 +2495,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     threads = 32 * ((pp.P == 32 ? 8 : 12) + 4);  // compute warps of the instance (see instance_kernel)
   } else if (inst.warp == 3) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 8 * (size_t)a.stages;
-  } else if (inst.warp == 2 || inst.warp == 4) {
+  } else if (inst.warp == 2) {
     smem = 1024 + (size_t)(a.stages + 2) * a.stage_bytes + 8 * 4 * (size_t)a.stages;
     threads = 32 * (1 + 3 * (inst.NT / 32));  // producer warp + one warp group per factor (max 3)
   } else {
@@ -2532,13 +2511,8 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     smem = 1024 + (size_t)a.stages * 65536 + 3 * 1024 + 80 * (size_t)a.stages;
     threads = 32 * (12 + 4);
     Kernel4Fn k10 = a.push.on ? kron_fused_gemm3c_kernel<12, true> : instance_kernel4(pp.variant);
-    static std::once_flag attr_once[2];
-    static cudaError_t attr_err[2] = {cudaSuccess, cudaSuccess};
-    const int ki = a.push.on ? 1 : 0;
-    std::call_once(attr_once[ki], [&] {
-      attr_err[ki] = cudaFuncSetAttribute((const void *)k10, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    });
-    if (attr_err[ki] != cudaSuccess) return (int)attr_err[ki];
+    const int aerr = set_smem_attr((const void *)k10, 227 * 1024);  // per (kernel, device)
+    if (aerr != 0) return aerr;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2556,31 +2530,14 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     k4<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, a);
     return (int)cudaGetLastError();
   }
-  if (inst.warp == 2 || inst.warp == 4) {
-    KernelPFn kp = instance_pipe(pp.variant);
+  if (inst.warp == 2) {
+    KernelFn kp = instance_pipe(pp.variant);
     const int slots = kernel_slots((const void *)kp, threads, smem);
     if (slots < 1) return (int)cudaErrorInvalidConfiguration;
-    if (inst.warp == 2) {
-      int64_t grid = slots;
-      if (grid > a.ntiles) grid = a.ntiles;
-      kp<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a, tin2, tout2);
-      return (int)cudaGetLastError();
-    }
-    // pair: both passes co-resident (cooperative launch), one CTA of each role per slot
-    int64_t half = slots / 2;
-    if (half > a.ntiles) half = a.ntiles;
-    if (half < 1) return (int)cudaErrorInvalidConfiguration;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)(2 * half));
-    cfg.blockDim = dim3((unsigned)threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = (cudaStream_t)stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, kp, tin, tout, a, tin2, tout2);
+    int64_t grid = slots;
+    if (grid > a.ntiles) grid = a.ntiles;
+    kp<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a);
+    return (int)cudaGetLastError();
   }
   KernelFn k = instance_kernel(pp.variant);
   if (a.push.on) {  // v6 with the fused exchange (same tiling, push epilogue)

@@ -105,8 +105,8 @@ int launch_t(const PassPlan &pp, int64_t M, const void *in, void *out, const voi
   }
   GenFn<T> k = pick<T>(pp.P);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return (int)e;
+    const int e = set_smem_attr((const void *)k, smem);
+    if (e != 0) return e;
   }
   const int64_t S = pp.W_in / pp.P, ntiles = M * ((S + TS - 1) / TS);
   int64_t grid = ntiles < 148 * 8 ? ntiles : 148 * 8;

@@ -30,8 +30,6 @@ struct PassPlan {
   int variant = -1;  // fused: kernel instance id; gemm: instance id
   int stages = 2;
   int nout = 0;  // output staging buffers (warp-chain fused kernel)
-  int pair = 0;       // 1: L2-fused pair of passes (factors first .. first-2nf+1), one cooperative launch
-  int ring_rows = 0;  // pair: rows of the L2-resident ring between the two passes
   int src = BUF_X, dst = BUF_Y;
 };
 
@@ -43,7 +41,6 @@ struct Plan {
   std::vector<PassPlan> passes;
   int nws = 0;             // workspace buffers (0, 1 or 2)
   int64_t ws_elems = 0;    // elements per workspace buffer
-  int64_t aux_bytes = 0;   // extra workspace after the buffers (L2-fused pair: ring + row counters)
 };
 
 // Builds the plan (host only).  Returns KRON_OK or a validation error.
@@ -60,21 +57,33 @@ struct PlanPolicy {
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
                         int64_t lead = 1, const PlanPolicy &policy = PlanPolicy());
 size_t plan_ws_bytes(const Plan &plan);
-// Distributed P2P push (NEXT-1): the LAST pass of a plan writes every output value straight to its
-// StoreGPUTile position in the destination rank's buffer (peer memory).  Output column c of the local
-// block goes to rank d = c / B at column ((e / rho) * GK + me) * rho + e % rho, e = c % B, of a row of
-// width wd.  Only kernels whose store path implements it (plan_push_ok) are driven this way.
+// Distributed rounds (Algorithm 2).  Two hooks let a round's local passes do the exchange's
+// data movement themselves, so no separate pack / StoreGPUTile pass touches HBM:
+//
+// PushArgs — the LAST pass of a plan writes every output value to a per-destination buffer instead of Y.
+// Output column c of the local block goes to rank d = c / B at column ((e / rho) * GK + me) * rho + e % rho,
+// e = c % B, of a row of width wd.  P2P (backend 2): dst[d] = peer d's heap half, rho = the round's run
+// length (StoreGPUTile over NVLink, NEXT-1).  NCCL / virtual (backends 0, 1): dst[d] = this rank's
+// destination-major send block d, rho = B, GK = 1, me = 0, wd = B (the pack fused into the epilogue).
 constexpr int kMaxPush = 8;
 struct PushArgs {
   void *dst[kMaxPush] = {};
   int64_t B = 0, rho = 0, wd = 0;
   int GK = 0, me = 0, on = 0;
 };
-bool plan_push_ok(const Plan &plan);
+// InRemap — the FIRST pass of a plan reads its input in place from an all-to-all receive buffer
+// recv[src][m][e*rho + t] through a 5-D tensor map whose coordinate order is the StoreGPUTile layout
+// (local column (e*GK + src)*rho + t, Alg 2): the remap happens in the TMA engine.
+struct InRemap {
+  int64_t rho = 0;
+  int GK = 0, on = 0;
+};
+bool plan_push_ok(const Plan &plan, const PushArgs &push);
+bool plan_remap_ok(const Plan &plan, const InRemap &rin);
 void keep_pool_cached();  // default mem pool keeps freed blocks (stream-ordered workspaces)
-// Enqueue every pass of `plan` (F indexed like the plan's P/Q arrays); ws >= plan_ws_bytes bytes.
+// Enqueue passes [i0, i1) (i1 < 0: all) of `plan` (F indexed like the plan's P/Q arrays); ws >= plan_ws_bytes.
 kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, void *Y, void *ws, void *stream,
-                       const PushArgs *push = nullptr);
+                       const PushArgs *push = nullptr, const InRemap *rin = nullptr, int i0 = 0, int i1 = -1);
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype);
 
 // ---- fused small-P kernel family (fused.cu)
@@ -95,13 +104,17 @@ int fused_find(int dtype, int P, int warp);  // instance id or -1
 int launch_generic(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F,
                    void *stream);
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
-                 void *aux, void *stream, const PushArgs *push = nullptr);
+                 void *stream, const PushArgs *push = nullptr, const InRemap *rin = nullptr);
+// input-box geometry of a fused pass (lines of 128 bytes per TMA box); shared by launch_fused and plan_remap_ok
+int fused_box_lines(const PassPlan &pp, int dtype);
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 
 // resident CTA slots (SMs x CTAs per SM) for a kernel launch shape; sets the dynamic-smem attribute.
 // Cached per (kernel, block, smem, device).  fused.cu
 int kernel_slots(const void *fn, int threads, size_t smem);
+// raise the kernel's dynamic-smem limit on the current device (cached per (kernel, device)); cudaError_t
+int set_smem_attr(const void *fn, size_t smem);
 
 // tensor-map encoder (driver entry point fetched through the runtime); fused.cu
 bool tmap_available();

@@ -345,6 +345,14 @@ _lib.kron_dist_ctx_destroy.restype = ctypes.c_int
 _lib.kron_dist_ctx_destroy.argtypes = [ctypes.c_void_p]
 _lib.kron_dist_ctx_grid.restype = ctypes.c_int
 _lib.kron_dist_ctx_grid.argtypes = [ctypes.c_void_p, _i32p, _i32p]
+_lib.kron_dist_ctx_set.restype = ctypes.c_int
+_lib.kron_dist_ctx_set.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
+_lib.kron_dist_sync.restype = ctypes.c_int
+_lib.kron_dist_sync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+_lib.kron_dist_round_info.restype = ctypes.c_int
+_lib.kron_dist_round_info.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, ctypes.c_void_p,
+                                      ctypes.c_int32, _i32p, _i32p, _i32p]
+KRON_DIST_OPT_CHUNKS, KRON_DIST_OPT_FUSED_LAYOUT, KRON_DIST_OPT_P2P_PUSH = 1, 2, 3
 _lib.kron_matmul_dist.restype = ctypes.c_int
 _lib.kron_matmul_dist.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
                                   ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
@@ -354,9 +362,13 @@ class DistContext:
     """kron_dist_ctx_t.  backend "nccl": one rank per GPU; the ncclUniqueId is created by rank 0 and
     broadcast over the torch ProcessGroup `pg` (plumbing only).  backend "virtual": all GM*GK ranks of the
     grid live in this process on the current GPU (exchange = device copies).  GM = GK = 0: the paper's
-    grid rule."""
+    grid rule.  Options (identical on every rank): `chunks` row chunks per round (NCCL /
+    virtual: chunk c's all-to-all overlaps chunk c+1's passes), `fused` the fused send / receive layouts
+    (False = separate pack and remap kernels), `push` the P2P backend's fused push rounds (None = the
+    library default, fixed at creation)."""
 
-    def __init__(self, backend="nccl", world_size=None, rank=None, GM=0, GK=0, pg=None):
+    def __init__(self, backend="nccl", world_size=None, rank=None, GM=0, GK=0, pg=None, chunks=None, fused=None,
+                 push=None):
         self.handle = ctypes.c_void_p()
         if backend == "nccl":
             import torch.distributed as dist
@@ -391,6 +403,24 @@ class DistContext:
         gm, gk = ctypes.c_int32(), ctypes.c_int32()
         _check(_lib.kron_dist_ctx_grid(self.handle, ctypes.byref(gm), ctypes.byref(gk)), "kron_dist_ctx_grid")
         self.GM, self.GK = gm.value, gk.value
+        for opt, val in ((KRON_DIST_OPT_CHUNKS, chunks), (KRON_DIST_OPT_FUSED_LAYOUT, fused),
+                         (KRON_DIST_OPT_P2P_PUSH, push)):
+            if val is not None:
+                _check(_lib.kron_dist_ctx_set(self.handle, opt, int(val)), "kron_dist_ctx_set")
+
+    def sync(self, stream=None, timeout_ms: int = 120000) -> None:
+        """kron_dist_sync: wait for `stream`, polling NCCL's asynchronous errors (raises KronError with
+        KRON_ERR_NCCL / KRON_ERR_CUDA on a failed or stuck collective or a P2P barrier that gave up)."""
+        _check(_lib.kron_dist_sync(self.handle, _stream_ptr(stream), int(timeout_ms)), "kron_dist_sync")
+
+    def round_info(self, M, P, Q, dtype):
+        """[(fused_send, fused_recv)] per round for this context's grid (host only)."""
+        Pa, Qa = _shape_arrays(P, Q)
+        n = ctypes.c_int32()
+        fs, fr = (ctypes.c_int32 * 64)(), (ctypes.c_int32 * 64)()
+        _check(_lib.kron_dist_round_info(M, len(P), Pa, Qa, dtype_code(dtype), self.handle, 64, ctypes.byref(n),
+                                         fs, fr), "kron_dist_round_info")
+        return [(bool(fs[i]), bool(fr[i])) for i in range(n.value)]
 
     def ensure_heap(self, nbytes: int) -> None:
         """P2P backend: (re)reserve the symmetric heap if it is smaller than `nbytes` and map the peers'
@@ -431,30 +461,47 @@ class DistContext:
             pass
 
 
-def matmul_dist(M, X_local, Fs, ctx: DistContext, out=None, stream=None):
-    """kron_matmul_dist().  nccl backend: X_local is this rank's block X[gM rows, gK K-block]; returns
+def matmul_dist(M, X_local, Fs, ctx: DistContext, out=None, stream=None, check: bool = False):
+    """kron_matmul_dist().  nccl / p2p backends: X_local is this rank's block X[gM rows, gK K-block]; returns
     Y_local = Y[gM rows, gK L-block].  virtual backend: X_local is a list of every rank's block (rank
-    order gM*GK + gK); returns the list of Y_local blocks."""
+    order gM*GK + gK); returns the list of Y_local blocks.  check=True waits for the result and raises on an
+    asynchronous NCCL error or a P2P barrier timeout (ctx.sync)."""
     import torch
+    if not Fs:
+        raise ValueError("at least one factor")
     P = [int(f.shape[0]) for f in Fs]
     Q = [int(f.shape[1]) for f in Fs]
-    L = 1
-    for q in Q:
-        L *= q
+    K, L = 1, 1
+    for p, q in zip(P, Q):
+        K, L = K * p, L * q
+    xs = list(X_local) if isinstance(X_local, (list, tuple)) else [X_local]
+    nblk = ctx.GM * ctx.GK if ctx.backend == "virtual" else 1
+    if len(xs) != nblk:
+        raise ValueError(f"{ctx.backend} backend expects {nblk} X block(s), got {len(xs)}")
+    if M % ctx.GM or K % ctx.GK or L % ctx.GK:
+        raise ValueError(f"grid {ctx.GM}x{ctx.GK} does not divide M={M}, K={K}, L={L}")
+    xshape, shape = (M // ctx.GM, K // ctx.GK), (M // ctx.GM, L // ctx.GK)
+    dt, dev = xs[0].dtype, xs[0].device
+    for x in xs:
+        if not x.is_cuda or not x.is_contiguous() or x.dtype != dt or x.device != dev or tuple(x.shape) != xshape:
+            raise ValueError(f"X blocks must be contiguous {dt} CUDA tensors of shape {xshape} on {dev}")
+    for f in Fs:
+        if not f.is_cuda or not f.is_contiguous() or f.dtype != dt or f.device != dev or f.dim() != 2:
+            raise ValueError(f"factors must be contiguous 2-D {dt} CUDA tensors on {dev}")
+    if out is None:
+        outs = [torch.empty(shape, dtype=dt, device=dev) for _ in xs]
+    else:
+        outs = list(out) if isinstance(out, (list, tuple)) else [out]
+        if len(outs) != len(xs):
+            raise ValueError(f"expected {len(xs)} output block(s), got {len(outs)}")
+        for y in outs:
+            if not y.is_cuda or not y.is_contiguous() or y.dtype != dt or y.device != dev or tuple(y.shape) != shape:
+                raise ValueError(f"output blocks must be contiguous {dt} CUDA tensors of shape {shape} on {dev}")
     Pa, Qa = _shape_arrays(P, Q)
     Fp = (ctypes.c_void_p * len(Fs))(*[f.data_ptr() for f in Fs])
-    xs = X_local if isinstance(X_local, (list, tuple)) else [X_local]
-    for x in xs:
-        if not x.is_cuda or not x.is_contiguous():
-            raise ValueError("X blocks must be contiguous CUDA tensors")
-    shape = (M // ctx.GM, L // ctx.GK)
-    if out is None:
-        outs = [torch.empty(shape, dtype=xs[0].dtype, device=xs[0].device) for _ in xs]
-    else:
-        outs = out if isinstance(out, (list, tuple)) else [out]
     if ctx.backend == "p2p":
         need = ctypes.c_size_t()
-        _check(_lib.kron_dist_p2p_heap_bytes(M, len(P), Pa, Qa, dtype_code(xs[0].dtype), ctx.GM, ctx.GK,
+        _check(_lib.kron_dist_p2p_heap_bytes(M, len(P), Pa, Qa, dtype_code(dt), ctx.GM, ctx.GK,
                                              ctypes.byref(need)), "kron_dist_p2p_heap_bytes")
         ctx.ensure_heap(need.value)
     if ctx.backend == "virtual":
@@ -463,6 +510,8 @@ def matmul_dist(M, X_local, Fs, ctx: DistContext, out=None, stream=None):
         xarg, yarg = ctypes.cast(xp, ctypes.c_void_p), ctypes.cast(yp, ctypes.c_void_p)
     else:
         xarg, yarg = xs[0].data_ptr(), outs[0].data_ptr()
-    _check(_lib.kron_matmul_dist(M, len(P), Pa, Qa, xarg, Fp, yarg, dtype_code(xs[0].dtype), ctx.handle,
+    _check(_lib.kron_matmul_dist(M, len(P), Pa, Qa, xarg, Fp, yarg, dtype_code(dt), ctx.handle,
                                  _stream_ptr(stream)), "kron_matmul_dist")
+    if check:
+        ctx.sync(stream)
     return outs if isinstance(X_local, (list, tuple)) else outs[0]

@@ -103,19 +103,6 @@ def test_workspace_sizes(kron):
     assert ws >= 10 * 64 * 8
 
 
-def test_l2_pair_plan_opt_in():
-    # the experimental L2-fused pair (KRON_PAIR=1) plans one launch for both groups of config B with a
-    # 32-row ring; checked in a fresh process because plans are cached per process
-    import subprocess
-    import sys
-    code = ("from paper_2401_10187_b200 import kron; "
-            "print(kron.plan_describe(1024,[8]*6,[8]*6,'float32'), kron.workspace_size(1024,[8]*6,[8]*6,'float32'), "
-            "kron.plan_cost(1024,[8]*6,[8]*6,'float32')[0])")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=ROOT,
-                         env={**os.environ, "KRON_PAIR": "1"}).stdout.strip()
-    assert out == f"[(6, 6, 'fused')] {32 * 8 ** 6 * 4 + 2 * 1024 * 4} {float(2 * 4 * 1024 * 8 ** 6 + 6 * 4 * 64)}"
-
-
 def test_grid_rule_matches_oracle(kron):
     for G in [1, 2, 4, 8, 16, 32, 64]:
         assert kron.grid_rule(G) == oracle.grid(G)
@@ -222,3 +209,23 @@ def test_host_path_argument_errors(kron):
     Fp = (ctypes.c_void_p * 2)(1, 1)
     assert lib.kron_matmul_host(4, 2, Pa, Pa, 1, Fp, 1, 0, -1, None) == 1           # chunk_rows < 0
     assert lib.kron_matmul_host(0, 2, Pa, Pa, None, None, None, 0, 0, None) == 0     # M = 0: no-op
+
+
+def test_dist_round_info_fused_layouts(kron):
+    # host-only: which rounds of backends 0 / 1 write the send buffer from the last pass's epilogue (fused
+    # pack) and read the previous receive buffer through the StoreGPUTile-ordered tensor map (fused remap)
+    ctx = kron.DistContext("virtual", GM=4, GK=2)
+    # config E on the 8-GPU paper grid: round 1 = v9 triple (no remap: it reads X), round 2 = v6 pair
+    assert ctx.round_info(4096, [16] * 5, [16] * 5, "float32") == [(True, False), (True, True)]
+    # C32 on {1,2}: two rounds of v6 P = 32 pairs
+    ctx2 = kron.DistContext("virtual", GM=1, GK=2)
+    assert ctx2.round_info(1024, [32] * 4, [32] * 4, "float32") == [(True, False), (True, True)]
+    # fp64 pairs (DMMA v5) have no pushing epilogue -> pack kernel, but read the receive buffer in place
+    assert ctx2.round_info(1024, [32] * 4, [32] * 4, "float64") == [(False, False), (False, True)]
+    # the fused layouts can be switched off (separate pack / StoreGPUTile kernels)
+    ctx3 = kron.DistContext("virtual", GM=1, GK=2, fused=False)
+    assert ctx3.round_info(1024, [32] * 4, [32] * 4, "float32") == [(False, False), (False, False)]
+    with pytest.raises(kron.KronError):
+        kron.DistContext("virtual", GM=1, GK=2, chunks=0)
+    for c in (ctx, ctx2, ctx3):
+        c.close()

@@ -26,8 +26,6 @@ def _free_port():
 
 
 def _worker(rank, world, port, GM, GK, M, P, Q, q, push=True):
-    if not push:
-        os.environ["KRON_P2P_NO_PUSH"] = "1"  # every round through the pull kernel
     import torch
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -39,7 +37,7 @@ def _worker(rank, world, port, GM, GK, M, P, Q, q, push=True):
         from paper_2401_10187_b200 import kron
         dev = torch.device("cuda:0")
         torch.cuda.set_device(dev)
-        ctx = kron.DistContext("p2p", GM=GM, GK=GK)
+        ctx = kron.DistContext("p2p", GM=GM, GK=GK, push=push)  # push=False: every round via the pull kernel
         gm, gk = ctx.coords()
         K, L = int(np.prod(P)), int(np.prod(Q))
         Ml, Kl, Ll = M // GM, K // GK, L // GK
@@ -49,7 +47,7 @@ def _worker(rank, world, port, GM, GK, M, P, Q, q, push=True):
             X = synth.matrix(M, K, seed, 0, mode, dt)
             Fs = synth.factors(P, Q, seed, mode, dt)
             xb = torch.from_numpy(np.ascontiguousarray(X[gm * Ml:(gm + 1) * Ml, gk * Kl:(gk + 1) * Kl])).to(dev)
-            Y = kron.matmul_dist(M, xb, [torch.from_numpy(f).to(dev) for f in Fs], ctx)
+            Y = kron.matmul_dist(M, xb, [torch.from_numpy(f).to(dev) for f in Fs], ctx, check=True)
             torch.cuda.synchronize()
             ref = oracle.alg1(X, Fs)[gm * Ml:(gm + 1) * Ml, gk * Ll:(gk + 1) * Ll]
             y = Y.cpu().numpy()
@@ -76,6 +74,8 @@ GRIDS = [
     (2, 2, 4, [8] * 4, [8] * 4),      # paper rule for 4 GPUs
     (1, 4, 2, [4] * 4, [4] * 4),      # Fig 8 {1,4}: K = 256, Local = 2
     (1, 2, 2, [8, 4, 4], [4, 8, 4]),  # mixed, non-square (scalar pull path)
+    (1, 2, 2, [2, 16, 16, 16, 8, 8], [2, 16, 16, 16, 8, 8]),      # v9 ends a round with rho = 1: no push
+    (1, 2, 2, [2, 16, 16, 8, 8, 4, 4], [2, 16, 16, 8, 8, 4, 4]),  # 3-pass push round (intermediates first)
 ]
 
 

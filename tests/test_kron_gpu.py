@@ -136,33 +136,6 @@ def test_workspace_variant_and_stream(kron, cuda_device):
         kron.matmul_ws(Xd, Fd, out, ws[:10])  # workspace too small -> KRON_ERR_SHAPE, nothing enqueued
 
 
-def test_l2_pair_experimental(cuda_device):
-    # the opt-in L2-fused pair (KRON_PAIR=1; plans are cached per process, so run in a fresh one)
-    import os
-    import subprocess
-    import sys
-    code = r"""
-import numpy as np, torch, oracle, synth
-from paper_2401_10187_b200 import kron
-M, P = 70, [8] * 6
-assert kron.plan_describe(M, P, P, 'float32') == [(6, 6, 'fused')]
-for mode, dt in (('int1', np.float32), ('urand', np.float32)):
-    X = synth.matrix(M, 8 ** 6, synth.SEED_BASE + 9, 0, mode, dt)
-    Fs = synth.factors(P, P, synth.SEED_BASE + 9, mode, dt)
-    Y = kron.matmul(torch.from_numpy(X).cuda(), [torch.from_numpy(f).cuda() for f in Fs]).cpu().numpy()
-    ref = oracle.alg1(X, Fs)
-    if mode == 'int1':
-        assert np.array_equal(Y, ref.astype(dt))
-    else:
-        assert float(np.max(np.abs(Y - ref) / np.abs(ref))) <= 1e-5
-print('pair ok')
-"""
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
-                         env={**os.environ, "KRON_PAIR": "1", "PYTHONPATH": root})
-    assert "pair ok" in res.stdout, res.stdout + res.stderr
-
-
 # ------------------------------------------------------------------ full BASELINE sizes, sampled rows
 
 FULL = [
