@@ -104,7 +104,7 @@ def test_dist_layout_errors(kron, cuda_device):
     with pytest.raises(ValueError, match="X block"):
         kron.matmul_dist(8, X[:7], Fs, ctx)  # the virtual backend needs GM*GK blocks
     with pytest.raises(ValueError, match="X blocks"):
-        kron.matmul_dist(8, [torch.zeros((2, 8 ** 3 // 2), device=cuda_device)] * 8, Fs, ctx)  # wrong block shape
+        kron.matmul_dist(8, X, Fs, ctx)  # blocks of 1 row, M/GM = 2 expected
     ctx.close()
     with pytest.raises(kron.KronError):
         kron.DistContext("virtual", world_size=6)  # grid rule does not yield 6 GPUs (G14)

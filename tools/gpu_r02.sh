@@ -11,9 +11,8 @@ if [ "$TESTS" = "1" ]; then
   tail -5 $OUT/pytest_gpu.log
 fi
 if [ "$BENCH" = "1" ]; then
-  /usr/bin/time -v timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err
+  T0=$(date +%s); timeout 900 python bench.py --gpus 1 --steps 20 --warmup 5 > $OUT/bench.json 2> $OUT/bench.err; echo "bench wall $(( $(date +%s) - T0 )) s"
   python tools/bench_summary.py $OUT/bench.json || tail -20 $OUT/bench.err
-  grep -E "Elapsed|Maximum resident" $OUT/bench.err
   timeout 600 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $OUT/ref.json 2> $OUT/ref.err; tail -c 400 $OUT/ref.json
 fi
 if [ "$NCU" = "1" ]; then
