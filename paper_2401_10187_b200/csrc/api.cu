@@ -34,11 +34,11 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   int64_t C = 1;
   for (int i = 0; i < k; ++i) C *= p;
   const int64_t E = inst.elems();
-  if (W % line || W % C || (C > E && inst.warp != 10)) return false;
+  if (W % line || W % C || (C > E && inst.warp != 10 && inst.warp != 12)) return false;
   const int64_t WC = W / C;
   if ((WC * es) % 16) return false;
-  if (inst.warp == 10) {
-    // v9 cluster pair: three factors, 8-chunk tiles split 4 + 4 over two CTAs (32-byte runs)
+  if (inst.warp == 10 || inst.warp == 12) {
+    // v9 / v10 cluster pair: three factors, 8-chunk tiles split 4 + 4 over two CTAs (32-byte runs)
     if (k != 3 || p != 16 || inst.dtype != KRON_F32 || W % (8 * C)) return false;
     pp->kind = KIND_FUSED;
     pp->nf = 3;
@@ -76,7 +76,7 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
     if (W * es >= (int64_t(1) << 32)) return false;  // 32-bit in-row store offsets
   }
-  if (inst.warp == 6 || inst.warp == 8) {
+  if (inst.warp == 6 || inst.warp == 8 || inst.warp == 11) {
     // warp-specialised fp32 chunk pairs: two factors, one tile row of whole chunk octets
     if (k != 2 || tileM != 1 || R % 8 || (R * C) != E) return false;
   }
@@ -91,9 +91,9 @@ bool fused_geometry(const FusedInstance &inst, int k, int64_t W, int64_t M, Pass
   }
   const int64_t stage = (tileM * tileK * es + 1023) / 1024 * 1024;
   int stages, nout = 0;
-  if (inst.warp == 5 || inst.warp == 6 || inst.warp == 8) {
+  if (inst.warp == 5 || inst.warp == 6 || inst.warp == 8 || inst.warp == 11) {
     // one warp-specialised CTA per SM (v8 keeps hi/lo splits of both factors)
-    stages = (int)((220 * 1024 - (inst.warp == 8 ? 4 : 2) * (int64_t)p * p * es) / stage);
+    stages = (int)((220 * 1024 - (inst.warp == 8 ? 4 : inst.warp == 11 ? 0 : 2) * (int64_t)p * p * es) / stage);
     if (stages > 8) stages = 8;
   } else if (inst.warp == 3) {
     stages = stage <= 32 * 1024 ? 3 : 2;
@@ -247,8 +247,8 @@ bool plan_push_ok(const Plan &plan, const PushArgs &push) {
   if (pp.kind != KIND_FUSED) return false;
   if (pp.W_out % push.B || push.B % push.rho || pp.W_out / push.B > kMaxPush) return false;
   const FusedInstance &fi = fused_instance(pp.variant);
-  if (fi.warp == 10) return push.rho % 4 == 0 && push.B % 4 == 0 && push.wd % 4 == 0;
-  return fi.warp == 6 && fi.dtype == KRON_F32 && (fi.P == 16 || fi.P == 32);
+  if (fi.warp == 10 || fi.warp == 12) return push.rho % 4 == 0 && push.B % 4 == 0 && push.wd % 4 == 0;
+  return (fi.warp == 6 || fi.warp == 11) && fi.dtype == KRON_F32 && (fi.P == 16 || fi.P == 32);
 }
 
 // The remapped input view needs every TMA box of the first pass to cover whole runs of rho elements, or
@@ -317,10 +317,15 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const int p = P[f - 1], q = Q[f - 1];
     const int64_t W = plan->W[f];
     const bool dmma_ok = policy.dmma && !getenv("KRON_NO_DMMA");
-    auto allowed = [&](int kind) { return (policy.kinds >> kind) & 1u; };
+    // KRON_KINDS_MASK (experiments only): restrict the kernel families of every plan (hex bit mask)
+    static const unsigned env_mask = getenv("KRON_KINDS_MASK") ? (unsigned)strtoul(getenv("KRON_KINDS_MASK"), nullptr, 16)
+                                                               : ~0u;
+    auto allowed = [&](int kind) { return (policy.kinds >> kind) & (env_mask >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
     const int inst_t = (tf32x3 && p == q && allowed(8)) ? fused_find(dtype, p, 8) : -1;
     const int inst_3 = (p == q && allowed(10)) ? fused_find(dtype, p, 10) : -1;
+    const int inst_3c = (p == q && allowed(12)) ? fused_find(dtype, p, 12) : -1;  // v10 triple
+    const int inst_sc = (p == q && allowed(11)) ? fused_find(dtype, p, 11) : -1;  // v10 pair
     int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     if (inst_s >= 0 && policy.short_tiles && dtype == KRON_F32 && p == 16) inst_s = 35;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
@@ -357,9 +362,11 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_3c >= 0 && fused_geometry(fused_instance(inst_3c), k, W, Mp, pp)) return inst_3c;
         if (inst_3 >= 0 && fused_geometry(fused_instance(inst_3), k, W, Mp, pp)) return inst_3;
         if (inst_t >= 0 && fused_geometry(fused_instance(inst_t), k, W, Mp, pp)) return inst_t;
         if (inst_d >= 0 && fused_geometry(fused_instance(inst_d), k, W, Mp, pp)) return inst_d;
+        if (inst_sc >= 0 && fused_geometry(fused_instance(inst_sc), k, W, Mp, pp)) return inst_sc;
         if (inst_s >= 0 && fused_geometry(fused_instance(inst_s), k, W, Mp, pp)) return inst_s;
         if (inst_g >= 0 && fused_geometry(fused_instance(inst_g), k, W, Mp, pp)) return inst_g;
         if (inst_p >= 0 && fused_geometry(fused_instance(inst_p), k, W, Mp, pp)) return inst_p;
@@ -688,8 +695,10 @@ kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x7FFu;
-  const unsigned kinds[] = {all, all & ~(1u << 10), all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
+  const unsigned all = 0x1FFFu;
+  const unsigned v10 = (1u << 11) | (1u << 12);  // constant-bank kernels vs their round-1 shared-memory twins
+  const unsigned kinds[] = {all, all & ~v10, all & ~(1u << 12), all & ~(1u << 11), all & ~((1u << 10) | (1u << 12)),
+                            all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
                             all & ~((1u << 3) | (1u << 5) | (1u << 6) | (1u << 7)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
   std::vector<Plan> cands;
@@ -826,9 +835,10 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
                                   "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel", "kron_fused_tf32x3_kernel",
-                                  "kron_fused_kernel",         "kron_fused_gemm3c_kernel"};
+                                  "kron_fused_kernel",         "kron_fused_gemm3c_kernel",
+                                  "kron_fused_gemm2ws_kernel", "kron_fused_gemm3c_kernel"};
     const int w = fused_instance(pp.variant).warp;
-    k = (w >= 0 && w < 11) ? names[w] : "kron_fused_kernel";
+    k = (w >= 0 && w < 13) ? names[w] : "kron_fused_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

@@ -63,6 +63,18 @@ struct FusedArgs {
   int rmp_GK;
 };
 
+// ------------------------------------------------------------------ constant-bank factors (round 2)
+// The factors of a pass are copied (stream-ordered, device to device) into a constant-bank array before
+// the launch; the kernels' FFMA2s then take their factor operand as a uniform register loaded by LDCU.128
+// from the constant cache — `FFMA2 R, R.F32x2, UR.F32, R` (two slices' element p, one factor value
+// broadcast).  Shared memory carries only the data and no register holds a factor: tools/microbench_cfma.cu
+// measured 72 TFLOP/s (97% of the FP32 peak) for this loop shape with 1-3 16x16 factors (3 KB; 8 KB of
+// factors drop to 50 TFLOP/s: the constant cache working set), profiles/r02_microbench_cfma.jsonl.
+// The arrays sit at fixed addresses (compile-time LDCU offsets: a runtime slot offset makes ptxas fall back
+// to per-thread LDC); one array per kernel family, reused in stream order (see cslot_acquire).
+__constant__ float c_fac2[2 * 256];  // v10 pair (F1, F2)
+__constant__ float c_fac3[3 * 256];  // v10 triple (F1, F2, F3)
+
 // One input box of a fused pass (rows x 128-byte lines from `line`): the plain 3-D map, or the 5-D
 // StoreGPUTile view of a receive buffer (Alg 2 line 685 done by the TMA engine's address generation).
 __device__ __forceinline__ void load_in(const FusedArgs &a, void *dst, const CUtensorMap *m, uint64_t *bar, int line,
@@ -1074,6 +1086,126 @@ __global__ void __launch_bounds__(NW * 32, MINB) kron_fused_gemm2_kernel(const _
   }
 }
 
+// ------------------------------------------------------------------ constant-bank 16x16 chunk steps (v10)
+//
+// Every FFMA2 below takes its factor operand from a uniform register (LDCU from the constant bank): the
+// factor index may depend only on loop counters, never on the lane, so each warp-level FFMA2 uses ONE
+// factor value (or pair) — lanes differ only in the data they hold.  The calling branch must be provably
+// warp-uniform (warp index via __shfl_sync) for the compiler to use the uniform datapath.
+//
+// cb_pair16: four 256-element chunks [d1][d2] (chunks g0 .. g0+3) of a 128B-swizzled stage, both factors of
+// a 16x16 pair applied in place:
+//   step 1 (F1 on d2): lane = row r = lane % 16 of chunks g0 + lane / 16 and g0 + lane / 16 + 2;
+//          x = a row's 16 values (4 conflict-free LDS.128 on the TMA layout), out[q] = sum_p x[p] F1[p][q] as
+//          128 FFMA2 per row with x broadcast and a factor PAIR (F1[p][q], F1[p][q+1]) from a uniform register
+//          pair, written back over the row with the chunk's granule XOR gx(g) (so step 2's loads of
+//          consecutive chunks fall in different bank halves);
+//   step 2 (F2 on d1): lane = column pair (2j, 2j+1), j = lane % 8, of chunk g0 + lane / 8; x2[s] = the pair
+//          in row s (LDS.64), OUT[q2][q1] = sum_s F2[s][q2] Z[s][q1] as 256 FFMA2 on the column pair with a
+//          factor broadcast, written back over the same column pair (u = q2*16 + q1 at swz128(u*4) ^ gx).
+// 32 FMAs per element, 8 LDS.128 + 8 STS.128 + 16 LDS.64 + 16 STS.64 per lane for 512 FFMA2, whose factor
+// operands come from 128 LDCU.128.
+__device__ __forceinline__ void cb_pair16(unsigned char *buf, uint32_t g0, int lane, const float *F1, const float *F2) {
+  const float4 *F1v = reinterpret_cast<const float4 *>(F1), *F2v = reinterpret_cast<const float4 *>(F2);
+  {
+    const int sl = lane & 15;
+    uint32_t rb[2], gx[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const uint32_t g = g0 + (uint32_t)(lane >> 4) + 2u * h;
+      rb[h] = g * 1024u;
+      gx[h] = pipe_gx<8, 4>(g);
+    }
+    float x[2][16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const float4 t = *reinterpret_cast<const float4 *>(buf + rb[h] + swz128((uint32_t)(sl * 16 + 4 * v) * 4u));
+        x[h][4 * v] = t.x; x[h][4 * v + 1] = t.y; x[h][4 * v + 2] = t.z; x[h][4 * v + 3] = t.w;
+      }
+    float2 acc[2][8];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[h][j] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < 16; ++p)
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        const float4 f = F1v[p * 4 + j4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float2 xx = make_float2(x[h][p], x[h][p]);
+          acc[h][2 * j4] = __ffma2_rn(xx, make_float2(f.x, f.y), acc[h][2 * j4]);
+          acc[h][2 * j4 + 1] = __ffma2_rn(xx, make_float2(f.z, f.w), acc[h][2 * j4 + 1]);
+        }
+      }
+    __syncwarp();  // the gx-XOR'd write-back of a row lands on its neighbour row's bytes
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 4; ++v)
+        *reinterpret_cast<float4 *>(buf + rb[h] + (swz128((uint32_t)(sl * 16 + 4 * v) * 4u) ^ gx[h])) =
+            make_float4(acc[h][2 * v].x, acc[h][2 * v].y, acc[h][2 * v + 1].x, acc[h][2 * v + 1].y);
+  }
+  __syncwarp();
+  {
+    const uint32_t g = g0 + (uint32_t)(lane >> 3), j = (uint32_t)(lane & 7);
+    unsigned char *ch = buf + g * 1024u;
+    const uint32_t gx = pipe_gx<8, 4>(g);
+    float2 x2[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      x2[r] = *reinterpret_cast<const float2 *>(ch + (swz128((uint32_t)(r * 16) * 4u + j * 8u) ^ gx));
+    float2 acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+#pragma unroll
+      for (int q4 = 0; q4 < 4; ++q4) {
+        const float4 f = F2v[r * 4 + q4];
+        acc[4 * q4] = __ffma2_rn(x2[r], make_float2(f.x, f.x), acc[4 * q4]);
+        acc[4 * q4 + 1] = __ffma2_rn(x2[r], make_float2(f.y, f.y), acc[4 * q4 + 1]);
+        acc[4 * q4 + 2] = __ffma2_rn(x2[r], make_float2(f.z, f.z), acc[4 * q4 + 2]);
+        acc[4 * q4 + 3] = __ffma2_rn(x2[r], make_float2(f.w, f.w), acc[4 * q4 + 3]);
+      }
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      *reinterpret_cast<float2 *>(ch + (swz128((uint32_t)(q * 16) * 4u + j * 8u) ^ gx)) = acc[q];
+  }
+}
+
+// cb_top16: the third factor of a 16x16 triple on a 4096-element chunk of 16 subchunks (phase-1 layout:
+// element (k, col) at k*1024 + (swz128(col*4) ^ gx(k))): lane = column pair c, c + 1; OUT[q][c] =
+// sum_k F3[k][q] S[k][c] as 256 FFMA2 with a factor broadcast, in place (same layout, rows q; each lane owns
+// its column pair in every row, so no lane waits for another).
+__device__ __forceinline__ void cb_top16(unsigned char *cb, uint32_t c, const float *F3) {
+  const float4 *F3v = reinterpret_cast<const float4 *>(F3);
+  const uint32_t co = swz128(c * 4u);
+  float2 x2[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+    x2[k] = *reinterpret_cast<const float2 *>(cb + (uint32_t)k * 1024u + (co ^ pipe_gx<8, 4>((uint32_t)k)));
+  float2 acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int k = 0; k < 16; ++k)
+#pragma unroll
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const float4 f = F3v[k * 4 + q4];
+      acc[4 * q4] = __ffma2_rn(x2[k], make_float2(f.x, f.x), acc[4 * q4]);
+      acc[4 * q4 + 1] = __ffma2_rn(x2[k], make_float2(f.y, f.y), acc[4 * q4 + 1]);
+      acc[4 * q4 + 2] = __ffma2_rn(x2[k], make_float2(f.z, f.z), acc[4 * q4 + 2]);
+      acc[4 * q4 + 3] = __ffma2_rn(x2[k], make_float2(f.w, f.w), acc[4 * q4 + 3]);
+    }
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    *reinterpret_cast<float2 *>(cb + (uint32_t)q * 1024u + (co ^ pipe_gx<8, 4>((uint32_t)q))) = acc[q];
+}
+
 // ------------------------------------------------------------------ fp32 two-factor chunks, warp-specialised (v6)
 //
 // The v4 sandwich OUT = F2^T . (X . F1) per P x P chunk (P = 16 / 32, fp32), with every chunk owned by
@@ -1094,7 +1226,7 @@ __device__ __forceinline__ T *push_dst(const FusedArgs &a, int rb, int64_t col) 
   return reinterpret_cast<T *>(a.push.dst[d]) + (int64_t)rb * a.push.wd + tcol;
 }
 
-template <int P, int NCW, int RM, int RN, int VA, int KU = 1, bool PUSH = false>
+template <int P, int NCW, int RM, int RN, int VA, int KU = 1, bool PUSH = false, bool CB = false>
 __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                               const __grid_constant__ CUtensorMap tm_out,
                                                                               const FusedArgs a) {
@@ -1102,7 +1234,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
   constexpr int ES = 4, LINE = 32, C = P * P, PE = P * ES;
   constexpr int NSW = 4;
   constexpr int L1 = (P / RM) * (P / RN);  // lanes per chunk
-  constexpr int CPG = 32 / L1;             // chunks per warp (one work unit)
+  constexpr int CPG = CB ? 4 : 32 / L1;    // chunks per warp (one work unit)
+  static_assert(!CB || P == 16, "constant-bank pairs are P = 16");
   const int UPT = a.R / CPG;               // work units per tile
   constexpr uint32_t CE = C * ES;          // chunk bytes (a multiple of 1024)
   static_assert(L1 <= 32 && 32 % L1 == 0, "lane tiling");
@@ -1113,9 +1246,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
   unsigned char *F2Ts = reinterpret_cast<unsigned char *>(F1s + C);          // [q2][s], 128B-swizzled
   uint64_t *full = reinterpret_cast<uint64_t *>(F2Ts + CE);
   uint64_t *cdone = full + a.stages, *empty = cdone + a.stages;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // provably warp-uniform
 
-  {
+  if constexpr (!CB) {
     const T *F1 = reinterpret_cast<const T *>(a.F[0]);
     const T *F2 = reinterpret_cast<const T *>(a.F[1]);
     for (int i = tid; i < C; i += (NCW + NSW) * 32) {
@@ -1148,7 +1281,20 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
   if (tid == 0)
     for (int it = 0; it < a.stages; ++it) issue_load(it);
 
-  if (warp < NCW) {
+  if (CB && warp < NCW) {
+    // v10 compute: each unit = two chunks through cb_pair16 (factors in the constant bank)
+    const float *F1c = c_fac2, *F2c = c_fac2 + C;
+    for (int un = warp;; un += NCW) {
+      const int it = un / UPT, cg = un % UPT;
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % a.stages;
+      mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
+      cb_pair16(base + (size_t)st * a.stage_bytes, (uint32_t)(cg * 4), lane, F1c, F2c);
+      __syncwarp();
+      mbar_arrive(&cdone[st]);  // every lane publishes its own writes
+    }
+  } else if (warp < NCW) {
     const int c1 = lane / L1, tau = lane % L1;
     const int sg = tau % (P / RM), q1g = tau / (P / RM);
     // A-operand rows sg + (P/RM)*i of a 128B-swizzled [P][P] matrix at a 1024-aligned base
@@ -1361,7 +1507,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
 // compute-sanitizer racecheck / synccheck / memcheck clean (tools/sanitize.py).
 // P2W: columns per lane in phase 2 (16: one unit = a 16 x 128 block, fewer shared loads per FMA than
 // 8: E's v9 pass 11.73 -> 11.62 ms)
-template <int NCW, bool PUSH = false, int P2W = 16>
+template <int NCW, bool PUSH = false, int P2W = 16, bool CB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
     kron_fused_gemm3c_kernel(const __grid_constant__ CUtensorMap tm_in, const FusedArgs a) {
   using T = float;
@@ -1369,7 +1515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   constexpr uint32_t CE = C1 * ES;                // subchunk bytes (1 KB)
   constexpr int NSW = 4, L1 = (P / RM) * (P / RN), CPG = 32 / L1;
   constexpr int SUB = 64;                         // subchunks per CTA tile (4 chunks of 4096)
-  constexpr int U1 = SUB / CPG, U2 = 2 * 64 / P2W, UPT = U1 + U2;  // phase-2 units: 8 * P2W columns each
+  constexpr int U1 = CB ? SUB / 4 : SUB / CPG, U2 = CB ? 16 : 2 * 64 / P2W, UPT = U1 + U2;  // phase-2 units
   constexpr uint32_t TB = SUB * CE;               // 64 KB per CTA tile
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -1381,12 +1527,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   uint64_t *p1 = full + S, *cdone = p1 + 4 * S, *empty = cdone + S, *rdy = empty + S;
   unsigned *scnt = reinterpret_cast<unsigned *>(rdy + S);  // store warps done with the stage
   constexpr int NST = NSW - 1;  // store warps; the last warp of the group signals the peer
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // provably warp-uniform
   const uint32_t rank = cluster_ctarank(), peer = rank ^ 1u;
   const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
   const int64_t groups = a.tiles_k;  // 8-chunk groups per row
 
-  {
+  if constexpr (!CB) {
     const T *F1 = reinterpret_cast<const T *>(a.F[0]);
     const T *F2 = reinterpret_cast<const T *>(a.F[1]);
     const T *F3 = reinterpret_cast<const T *>(a.F[2]);
@@ -1400,7 +1546,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      for (int t = 0; t < 4; ++t) mbar_init(&p1[4 * s + t], (CPG == 4 ? 4 : 16 / CPG) * 32);
+      for (int t = 0; t < 4; ++t) mbar_init(&p1[4 * s + t], (CB ? 4 : CPG == 4 ? 4 : 16 / CPG) * 32);
       mbar_init(&cdone[s], U2 * 32);       // every phase-2 lane of this CTA
       mbar_init(&rdy[s], 1);               // the peer's signal warp: its tile is computed
       mbar_init(&empty[s], NST * 32 + 1);  // every store lane of this CTA + the peer's last store warp
@@ -1424,7 +1570,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   if (tid == 0)
     for (int it = 0; it < S; ++it) issue_load(it);
 
-  if (warp < NCW) {
+  if (CB && warp < NCW) {
+    // v10 compute (factors in the constant bank): the compute warps form NCW / 4 groups of four; a group
+    // owns one 4096-element chunk at a time (chunks dealt round-robin to the groups across the tiles of the
+    // ring).  Warp i of the group runs phase 1 on subchunks 4i .. 4i+3 (cb_pair16), the group meets at a
+    // named barrier, then warp i runs phase 2 on columns 64i .. 64i+63 (cb_top16).  Equal work per warp
+    // and a hardware barrier: no warp idles on another chunk's phase 1 (round-1's unit order made a chunk's
+    // phase-2 warps wait for its phase-1 warps; ncu put 14% of the stall samples on that wait).
+    static_assert(NCW % 4 == 0, "groups of four compute warps");
+    constexpr int NG = NCW / 4;
+    const int grp = warp >> 2, wi = warp & 3;
+    const float *F1c = c_fac3, *F2c = c_fac3 + C1, *F3c = c_fac3 + 2 * C1;
+    for (int64_t ci = grp;; ci += NG) {
+      const int it = (int)(ci >> 2), t = (int)(ci & 3);
+      const int64_t tile = cid + (int64_t)it * ncl;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      unsigned char *buf = base + (size_t)st * TB;
+      mbar_wait(&full[st], par);
+      cb_pair16(buf, (uint32_t)(t * 16 + wi * 4), lane, F1c, F2c);
+      named_bar_sync(1 + grp, 128);  // the chunk's four phase-1 units are in shared memory
+      cb_top16(buf + (uint32_t)(t * 16) * CE, (uint32_t)(wi * 64 + 2 * lane), F3c);
+      __syncwarp();
+      mbar_arrive(&cdone[st]);  // every lane publishes its own writes (the signal warp relays to the peer)
+    }
+  } else if (warp < NCW) {
     // one warp-level P x P x P product with 128B-swizzled A rows arow[] (k in blocks of 8)
     auto gemm = [&](const unsigned char *A, const uint32_t (&arow)[RM], auto loadB, auto &acc) {
       constexpr int NN = sizeof(acc[0]) / sizeof(T);
@@ -2243,6 +2414,9 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 16, 256, 2, 6, 0},
     // v9: fp32 16 x 16 factor triples on a 2-CTA cluster (NEXT-2): id 36
     {KRON_F32, 16, 256, 2, 10, 0},
+    // v10 (round 2): the v6 P = 16 pair and the v9 triple with their factors in the constant bank
+    // (cb_pair16 / cb_top16 compute warps, same TMA rings and stream-out): ids 37 (pair), 38 (triple)
+    {KRON_F32, 16, 512, 2, 11, 0}, {KRON_F32, 16, 256, 2, 12, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -2255,6 +2429,7 @@ Kernel4Fn instance_kernel4(int i) {
     case 33: return kron_fused_dmma2g_kernel<8, 4>;
     case 34: return kron_fused_tf32x3_kernel<8, 4>;
     case 36: return kron_fused_gemm3c_kernel<12>;
+    case 38: return kron_fused_gemm3c_kernel<12, false, 16, true>;
     case 25: return kron_fused_gemm2_kernel<float, 16, 4, 8, 8, 2>;
     case 26: return kron_fused_gemm2_kernel<float, 32, 4, 8, 8, 2>;
     case 27: return kron_fused_gemm2_kernel<double, 16, 4, 8, 8, 1>;
@@ -2280,6 +2455,7 @@ KernelFn instance_kernel(int i) {
     // P = 32: 8 x 8 lane tiles on 8 compute warps (162 registers): C32 3.20 -> 3.10 ms per pass; P = 16 keeps
     // 4 x 8 tiles on 12 warps (8 x 8 measured 7.6 -> 8.4 ms on E's pair pass)
     case 31: case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2>;
+    case 37: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, false, true>;
     case 32: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
@@ -2381,6 +2557,53 @@ int kernel_slots(const void *fn, int threads, size_t smem) {
   cache[key] = slots;
   return slots;
 }
+
+// Constant-bank factor arrays (v10): one per kernel family and device.  A launch copies its factors into
+// the array on its stream (device to device) after waiting for the array's previous user (an event
+// recorded after that kernel), so launches on different streams never overwrite each other's factors; on
+// one stream the wait is implied by stream order (the copy follows the previous kernel anyway).  Inside a
+// stream capture the waits / records are skipped (an uncaptured event cannot be waited on); a captured
+// graph carries its own copy nodes, ordered before its kernels.
+namespace {
+struct CSlot {
+  std::mutex mu;
+  cudaEvent_t ev = nullptr;
+  bool used = false;
+};
+CSlot g_cslots[64][2];
+
+int cslot_acquire(cudaStream_t s, int kind, const void *const *F, int nf, int pp, bool *capturing) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || nf * pp > (kind ? 768 : 512)) return (int)cudaErrorInvalidValue;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) return (int)cudaGetLastError();
+  *capturing = cs != cudaStreamCaptureStatusNone;
+  CSlot &S = g_cslots[dev][kind];
+  {
+    std::lock_guard<std::mutex> lk(S.mu);
+    if (!S.ev && cudaEventCreateWithFlags(&S.ev, cudaEventDisableTiming) != cudaSuccess) return (int)cudaGetLastError();
+    if (S.used && !*capturing && cudaStreamWaitEvent(s, S.ev, 0) != cudaSuccess) return (int)cudaGetLastError();
+  }
+  for (int i = 0; i < nf; ++i) {
+    const cudaError_t e = kind ? cudaMemcpyToSymbolAsync(c_fac3, F[i], (size_t)pp * sizeof(float),
+                                                         (size_t)i * pp * sizeof(float), cudaMemcpyDeviceToDevice, s)
+                               : cudaMemcpyToSymbolAsync(c_fac2, F[i], (size_t)pp * sizeof(float),
+                                                         (size_t)i * pp * sizeof(float), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return (int)e;
+  }
+  return 0;
+}
+
+void cslot_release(cudaStream_t s, int kind, bool capturing) {
+  if (capturing) return;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CSlot &S = g_cslots[dev][kind];
+  std::lock_guard<std::mutex> lk(S.mu);
+  if (cudaEventRecord(S.ev, s) == cudaSuccess) S.used = true;
+}
+}  // namespace
 
 int fused_instance_count() { return kNumInstances; }
 const FusedInstance &fused_instance(int i) { return kInstances[i]; }
@@ -2490,7 +2713,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     smem = 1024 + (size_t)a.stages * a.stage_bytes + (inst.warp == 8 ? 4 : 2) * (size_t)pp.P * pp.P * es +
            24 * (size_t)a.stages;
     threads = 32 * (8 + 4);
-  } else if (inst.warp == 6) {
+  } else if (inst.warp == 6 || inst.warp == 11) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
     threads = 32 * ((pp.P == 32 ? 8 : 12) + 4);  // compute warps of the instance (see instance_kernel)
   } else if (inst.warp == 3) {
@@ -2503,14 +2726,23 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
            (((size_t)pp.nf * pp.P * pp.P * es + 15) & ~15) + 8 * (size_t)a.stages;
   }
   if (push && push->on) {
-    if ((inst.warp != 10 && inst.warp != 6) || push->GK > kMaxPush) return (int)cudaErrorInvalidValue;
+    if ((inst.warp != 10 && inst.warp != 6 && inst.warp != 11 && inst.warp != 12) || push->GK > kMaxPush)
+      return (int)cudaErrorInvalidValue;
     a.push = *push;
   }
-  if (inst.warp == 10) {
+  // v10: this launch's factors go to a constant-bank slot first (stream-ordered)
+  const int cslot = inst.warp == 12 ? 1 : inst.warp == 11 ? 0 : -1;
+  bool capturing = false;
+  if (cslot >= 0) {
+    const int err = cslot_acquire((cudaStream_t)stream, cslot, Fgroup, pp.nf, pp.P * pp.P, &capturing);
+    if (err != 0) return err;
+  }
+  if (inst.warp == 10 || inst.warp == 12) {
     // cluster pair: grid = 2 x clusters (one CTA per SM), a.ntiles = 8-chunk groups
     smem = 1024 + (size_t)a.stages * 65536 + 3 * 1024 + 80 * (size_t)a.stages;
     threads = 32 * (12 + 4);
-    Kernel4Fn k10 = a.push.on ? kron_fused_gemm3c_kernel<12, true> : instance_kernel4(pp.variant);
+    Kernel4Fn k10 = inst.warp == 12 ? (a.push.on ? kron_fused_gemm3c_kernel<12, true, 16, true> : instance_kernel4(pp.variant))
+                                    : (a.push.on ? kron_fused_gemm3c_kernel<12, true> : instance_kernel4(pp.variant));
     const int aerr = set_smem_attr((const void *)k10, 227 * 1024);  // per (kernel, device)
     if (aerr != 0) return aerr;
     int dev = 0, sms = 148;
@@ -2519,7 +2751,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     int64_t ncl = sms / 2;  // one CTA per SM (the smem footprint), clusters of two
     if (ncl > a.ntiles) ncl = a.ntiles;
     k10<<<(unsigned)(2 * ncl), threads, smem, (cudaStream_t)stream>>>(tin, a);
-    return (int)cudaGetLastError();
+    const int lerr = (int)cudaGetLastError();
+    if (cslot >= 0) cslot_release((cudaStream_t)stream, cslot, capturing);
+    return lerr;
   }
   if (inst.warp == 3 || inst.warp == 5 || inst.warp == 8) {
     Kernel4Fn k4 = instance_kernel4(pp.variant);
@@ -2540,15 +2774,19 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     return (int)cudaGetLastError();
   }
   KernelFn k = instance_kernel(pp.variant);
-  if (a.push.on) {  // v6 with the fused exchange (same tiling, push epilogue)
-    k = pp.P == 32 ? kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, true> : kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true>;
+  if (a.push.on) {  // v6 / v10 pair with the fused exchange (same tiling, push epilogue)
+    k = inst.warp == 11 ? kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true, true>
+        : pp.P == 32    ? kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, true>
+                        : kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true>;
   }
   const int slots = kernel_slots((const void *)k, threads, smem);
   if (slots < 1) return (int)cudaErrorInvalidConfiguration;
   int64_t grid = slots;
   if (grid > a.ntiles) grid = a.ntiles;
   k<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, tout, a);
-  return (int)cudaGetLastError();
+  const int lerr = (int)cudaGetLastError();
+  if (cslot >= 0) cslot_release((cudaStream_t)stream, cslot, capturing);
+  return lerr;
 }
 
 }  // namespace kron

@@ -47,7 +47,7 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0x7FFu;     // allowed fused kernel families (bit = FusedInstance::warp)
+  unsigned kinds = 0x1FFFu;    // allowed fused kernel families (bit = FusedInstance::warp)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
   bool operator==(const PlanPolicy &o) const {
