@@ -109,6 +109,14 @@ def ncu_traffic(config, kernel_prefix):
         return None, None
 
 
+def measured_bf16():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0 * 0.74  # nominal x the measured/nominal ratio of the pool's B200s (B200_PROFILING.md)
+
+
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as f:
@@ -346,6 +354,13 @@ def roofline_of(M, P, Q, es, alg_bytes, alg_flops, t_s, mode=None, kname=None):
     alu_src = "derived: 148 SM x 128 FP32 lanes x 2 x 1.965 GHz" + (" / 2 (FP64)" if es == 8 else "")
     if mode and kname == "kron_fused_tf32x3_kernel":
         alu_peak, alu_src = MMA_TF32_TFLOPS / 3, "measured mma.sync TF32 (profiles/r01_microbench_mma.jsonl) / 3"
+    if mode and kname == "kron_tc_pair_kernel":
+        # tcgen05 kind::tf32 = half the dense bf16 rate (nominal 1.1 vs 2.25 PF); the measured cuBLAS bf16 peak
+        # of MEASURED_PEAKS.json x 1/2, / 3 MMAs per product in the 3xTF32 mode
+        bf16 = measured_bf16()
+        alu_peak = bf16 / 2 / (3 if mode == "3xtf32" else 1)
+        alu_src = (f"measured bf16 {bf16} TF/s (MEASURED_PEAKS.json) x 1/2 (tf32/bf16 nominal ratio)" +
+                   (" / 3 (3xTF32)" if mode == "3xtf32" else ""))
     t_hbm, t_alu = alg_bytes / (hbm_peak * 1e9), alg_flops / (alu_peak * 1e12)
     if t_hbm >= t_alu:
         ach = alg_bytes / t_s / 1e9
@@ -431,8 +446,8 @@ def measure_single(kron, synth, torch, cfg_name, args, dev, rank, barrier, mode=
                  "timing": "CUDA events on the launching stream around each launch, mean over the timed steps",
                  "traffic": traffic, "traffic_source": tsrc})
     b_alg, f_alg = kron.plan_cost(M, P, Q, tdt, mode)
-    step_roof = roofline_of(M, P, Q, es, b_alg, f_alg, ms / args.steps / 1e3, mode,
-                            "kron_fused_tf32x3_kernel" if mode and "kron_fused_tf32x3_kernel" in kernels else None)
+    tc_k = [k for k in ("kron_tc_pair_kernel", "kron_fused_tf32x3_kernel") if mode and k in kernels]
+    step_roof = roofline_of(M, P, Q, es, b_alg, f_alg, ms / args.steps / 1e3, mode, tc_k[0] if tc_k else None)
     hbm_peak, _ = measured_peaks()
     alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
     t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12))
@@ -522,7 +537,8 @@ def run_single(args, kron, synth, torch, ws, rank, local, dev, barrier):
             "metric": METRIC, "value": res["value"], "unit": "GFLOP/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": res["dtype"],
-            **({"mode": "3xtf32 (fp32 data, TF32 split tensor-core MMAs; reported separately)"} if mode else {}),
+            **({"mode": {"3xtf32": "3xtf32 (fp32 data, split-operand TF32 tcgen05 MMAs; reported separately)",
+                         "tf32": "tf32 (fp32 data, TF32 tcgen05 MMAs; reported separately)"}[mode]} if mode else {}),
             "data": "synthetic (seeded counter-based U[0,1) X and factors, generated in HBM)",
             "config": {"workload": args.config, "M_per_gpu": M, "P": res["P"], "Q": res["Q"], "K": K, "L": L,
                        "plan": res["plan"], "kernels": res["kernels"], "autotune": res["autotune"],
@@ -679,8 +695,8 @@ def main():
                          "kernels over peer memory (NEXT-1, P:652)")
     ap.add_argument("--grid", default=None, help="GMxGK for the distributed path (default: the paper rule)")
     ap.add_argument("--chunks", type=int, default=2, help="row chunks per round (exchange / compute overlap)")
-    ap.add_argument("--mode", default=None, choices=["3xtf32"],
-                    help="fp32 configs only: the separately reported 3xTF32 tensor-core mode (NEXT-4)")
+    ap.add_argument("--mode", default=None, choices=["3xtf32", "tf32"],
+                    help="fp32 configs only: the separately reported tcgen05 tensor-core modes (NEXT-4)")
     ap.add_argument("--autotune", action=argparse.BooleanOptionalAction, default=True,
                     help="autotune the pass plan before warm-up (P:599-619); --no-autotune = static plan")
     ap.add_argument("--sweep", default=None, choices=["table3", "table4"],
@@ -722,9 +738,9 @@ def main():
 
     use_dist = args.dist if args.dist is not None else (ws > 1 or args.config in WEAK)
     if args.mode and use_dist:
-        ap.error("--mode 3xtf32 is a single-GPU mode")
+        ap.error("--mode is a single-GPU mode")
     if args.mode and CONFIGS[args.config][4] != "float32":
-        ap.error("--mode 3xtf32 applies to the fp32 configs (B, C32, E)")
+        ap.error("--mode applies to the fp32 configs (B, C32, E)")
     rc = (run_dist if use_dist else run_single)(args, kron, synth, torch, ws, rank, local, dev, barrier)
     if ws > 1:
         torch.distributed.destroy_process_group()

@@ -39,7 +39,7 @@ extern "C" {
  * 3xTF32 tensor-core mode: P = 32 factor pairs run on the warp MMA with the
  * split x = hi + lo per operand (~22-bit products, fp32 accumulation); every other pass uses the fp32
  * CUDA-core kernels.  Not the default: KRON_F32 is the reference fp32 arithmetic. */
-typedef enum { KRON_F32 = 0, KRON_F64 = 1, KRON_F32_3XTF32 = 2 } kron_dtype_t;
+typedef enum { KRON_F32 = 0, KRON_F64 = 1, KRON_F32_3XTF32 = 2, KRON_F32_TF32 = 3 } kron_dtype_t;
 
 typedef enum {
   KRON_OK = 0,

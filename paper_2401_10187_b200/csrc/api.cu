@@ -270,7 +270,8 @@ bool plan_remap_ok(const Plan &plan, const InRemap &rin) {
 
 kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   if (M < 0 || N < 1 || N > kMaxFactors || !P || !Q) return KRON_ERR_INVALID_ARG;
-  if (dtype != KRON_F32 && dtype != KRON_F64 && dtype != KRON_F32_3XTF32) return KRON_ERR_INVALID_ARG;
+  if (dtype != KRON_F32 && dtype != KRON_F64 && dtype != KRON_F32_3XTF32 && dtype != KRON_F32_TF32)
+    return KRON_ERR_INVALID_ARG;
   for (int i = 0; i < N; ++i)
     if (P[i] < 1 || Q[i] < 1) return KRON_ERR_INVALID_ARG;
   const int64_t lim = (int64_t)1 << 50;  // elements per row; beyond any HBM
@@ -293,9 +294,12 @@ kron_status_t validate(int64_t M, int N, const int32_t *P, const int32_t *Q, int
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *plan, int64_t lead,
                         const PlanPolicy &policy) {
   kron_status_t st = validate(M, N, P, Q, dtype);
-  // 3xTF32 mode: fp32 data; P = 32 pairs go to the tensor-core kernel, everything else as KRON_F32
+  // tensor-core modes (fp32 data, reported separately): P = 16 / 32 square pairs go to the tcgen05 pair kernel
+  // (3xTF32 also to round 1's mma.sync kernel for P = 32 when the tcgen05 kernel is masked), everything else
+  // runs as KRON_F32
   const bool tf32x3 = dtype == KRON_F32_3XTF32;
-  if (tf32x3) dtype = KRON_F32;
+  const int tcm = dtype == KRON_F32_3XTF32 ? 2 : dtype == KRON_F32_TF32 ? 1 : 0;
+  if (tcm) dtype = KRON_F32;
   if (st != KRON_OK) return st;
   if (lead < 1) return KRON_ERR_INVALID_ARG;
   plan->N = N;
@@ -323,6 +327,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     auto allowed = [&](int kind) { return (policy.kinds >> kind) & (env_mask >> kind) & 1u; };
     const int inst_d = (p == q && dmma_ok && allowed(5)) ? fused_find(dtype, p, 5) : -1;
     const int inst_t = (tf32x3 && p == q && allowed(8)) ? fused_find(dtype, p, 8) : -1;
+    const int inst_tc = (tcm && p == q && allowed(13)) ? fused_find(dtype, p, 13) : -1;
     const int inst_3 = (p == q && allowed(10)) ? fused_find(dtype, p, 10) : -1;
     const int inst_3c = (p == q && allowed(12)) ? fused_find(dtype, p, 12) : -1;  // v10 triple
     const int inst_sc = (p == q && allowed(11)) ? fused_find(dtype, p, 11) : -1;  // v10 pair
@@ -362,6 +367,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
       while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
       // largest group either kernel can tile; prefer the warp-chain kernel for each group size
       auto pick = [&](int k, PassPlan *pp) -> int {
+        if (inst_tc >= 0 && k == 2 && tc_geometry(p, tcm, W, pp)) return inst_tc;
         if (inst_3c >= 0 && fused_geometry(fused_instance(inst_3c), k, W, Mp, pp)) return inst_3c;
         if (inst_3 >= 0 && fused_geometry(fused_instance(inst_3), k, W, Mp, pp)) return inst_3;
         if (inst_t >= 0 && fused_geometry(fused_instance(inst_t), k, W, Mp, pp)) return inst_t;
@@ -695,10 +701,10 @@ kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x1FFFu;
+  const unsigned all = 0x3FFFu;
   const unsigned v10 = (1u << 11) | (1u << 12);  // constant-bank kernels vs their round-1 shared-memory twins
   const unsigned kinds[] = {all, all & ~v10, all & ~(1u << 12), all & ~(1u << 11), all & ~((1u << 10) | (1u << 12)),
-                            all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
+                            all & ~(1u << 13), all & ~((1u << 13) | v10), all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
                             all & ~((1u << 3) | (1u << 5) | (1u << 6) | (1u << 7)), (1u << 0) | (1u << 1)};
   const int caps[] = {kMaxFused, 3, 2, 1};
   std::vector<Plan> cands;
@@ -836,9 +842,10 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",
                                   "kron_fused_gemm2ws_kernel", "kron_fused_dmma2g_kernel", "kron_fused_tf32x3_kernel",
                                   "kron_fused_kernel",         "kron_fused_gemm3c_kernel",
-                                  "kron_fused_gemm2ws_kernel", "kron_fused_gemm3c_kernel"};
+                                  "kron_fused_gemm2ws_kernel", "kron_fused_gemm3c_kernel",
+                                  "kron_tc_pair_kernel"};
     const int w = fused_instance(pp.variant).warp;
-    k = (w >= 0 && w < 13) ? names[w] : "kron_fused_kernel";
+    k = (w >= 0 && w < 14) ? names[w] : "kron_fused_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

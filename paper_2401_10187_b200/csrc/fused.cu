@@ -2417,6 +2417,8 @@ const FusedInstance kInstances[] = {
     // v10 (round 2): the v6 P = 16 pair and the v9 triple with their factors in the constant bank
     // (cb_pair16 / cb_top16 compute warps, same TMA rings and stream-out): ids 37 (pair), 38 (triple)
     {KRON_F32, 16, 512, 2, 11, 0}, {KRON_F32, 16, 256, 2, 12, 0},
+    // tcgen05 tensor-core pairs (tc.cu, TF32 / 3xTF32 modes only): ids 39 (P = 16), 40 (P = 32)
+    {KRON_F32, 16, 512, 1, 13, 0}, {KRON_F32, 32, 512, 1, 13, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -2501,17 +2503,25 @@ bool tmap_available() {
   return g_encode != nullptr;
 }
 
-bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims, const uint64_t *strides,
-                 const uint32_t *box, bool swizzle128) {
+bool encode_tmap_sw(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims,
+                    const uint64_t *strides, const uint32_t *box, int swizzle_bytes) {
   load_encode();
   if (!g_encode) return false;
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUtensorMapSwizzle sw = swizzle_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                      : CU_TENSOR_MAP_SWIZZLE_NONE;
   CUresult r = g_encode(m, dtype == KRON_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64,
                         (cuuint32_t)rank, const_cast<void *>(gaddr), (const cuuint64_t *)dims,
-                        (const cuuint64_t *)strides, (const cuuint32_t *)box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                        (const cuuint64_t *)strides, (const cuuint32_t *)box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims, const uint64_t *strides,
+                 const uint32_t *box, bool swizzle128) {
+  return encode_tmap_sw(m, dtype, rank, gaddr, dims, strides, box, swizzle128 ? 128 : 0);
 }
 
 
@@ -2622,6 +2632,7 @@ int fused_box_lines(const PassPlan &pp, int dtype) {
 int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
                  void *stream, const PushArgs *push, const InRemap *rin) {
   const FusedInstance &inst = kInstances[pp.variant];
+  if (pp.tc_mode) return launch_tc(pp, M, in, out, Fgroup, stream);
   const int es = dtype == KRON_F32 ? 4 : 8;
   const int line = 128 / es;
   const int64_t W = pp.W_in, WC = W / pp.C, Wout = pp.W_out;

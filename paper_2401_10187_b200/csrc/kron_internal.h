@@ -31,6 +31,7 @@ struct PassPlan {
   int stages = 2;
   int nout = 0;  // output staging buffers (warp-chain fused kernel)
   int src = BUF_X, dst = BUF_Y;
+  int tc_mode = 0;  // fused pair on the tcgen05 tensor cores (tc.cu): 1 TF32, 2 3xTF32; 0 otherwise
 };
 
 struct Plan {
@@ -47,7 +48,7 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0x1FFFu;    // allowed fused kernel families (bit = FusedInstance::warp)
+  unsigned kinds = 0x3FFFu;    // allowed fused kernel families (bit = FusedInstance::warp)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
   bool operator==(const PlanPolicy &o) const {
@@ -108,6 +109,9 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 // input-box geometry of a fused pass (lines of 128 bytes per TMA box); shared by launch_fused and plan_remap_ok
 int fused_box_lines(const PassPlan &pp, int dtype);
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
+// tcgen05 fp32 pair (tc.cu, NEXT-4): geometry for P = 16 / 32 pairs in mode 1 (TF32) / 2 (3xTF32), and launch
+bool tc_geometry(int P, int mode, int64_t W, PassPlan *pp);
+int launch_tc(const PassPlan &pp, int64_t M, const void *in, void *out, const void *const *Fgroup, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
 
 // resident CTA slots (SMs x CTAs per SM) for a kernel launch shape; sets the dynamic-smem attribute.
@@ -118,6 +122,8 @@ int set_smem_attr(const void *fn, size_t smem);
 
 // tensor-map encoder (driver entry point fetched through the runtime); fused.cu
 bool tmap_available();
+bool encode_tmap_sw(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims,
+                    const uint64_t *strides, const uint32_t *box, int swizzle_bytes);  // 0 / 32 / 64 / 128
 bool encode_tmap(CUtensorMap *m, int dtype, int rank, const void *gaddr, const uint64_t *dims, const uint64_t *strides,
                  const uint32_t *box, bool swizzle128);
 

@@ -88,18 +88,19 @@ def _check(rc: int, what: str) -> None:
         raise KronError(rc, what)
 
 
-MODES = {None: None, "fp32": None, "3xtf32": 2}
+MODES = {None: None, "fp32": None, "3xtf32": 2, "tf32": 3}
 
 
 def dtype_code(dtype, mode=None) -> int:
-    """C-ABI dtype: 0 float32, 1 float64, 2 float32 data in the 3xTF32 tensor-core mode (mode="3xtf32")."""
+    """C-ABI dtype: 0 float32, 1 float64; float32 data in the separately reported tensor-core modes:
+    2 (mode="3xtf32", split operands, ~fp32 accuracy) and 3 (mode="tf32", plain TF32 products)."""
     s = str(dtype)
     if mode not in MODES:
-        raise ValueError(f"unknown mode {mode!r} (None or '3xtf32')")
+        raise ValueError(f"unknown mode {mode!r} (None, 'tf32' or '3xtf32')")
     if s.endswith("float32"):
-        return 2 if MODES[mode] == 2 else 0
+        return MODES[mode] if MODES[mode] is not None else 0
     if mode is not None and MODES[mode] is not None:
-        raise ValueError("the 3xTF32 mode applies to float32 data only")
+        raise ValueError("the tensor-core modes apply to float32 data only")
     if s.endswith("float64"):
         return 1
     raise TypeError(f"Kron-Matmul supports float32 and float64, got {dtype}")

@@ -165,15 +165,21 @@ def test_plan_kernels(kron):
     assert lib.kron_plan_kernel(16, 2, Pa, Pa, 0, 5, buf, 8) == 1   # no such pass
 
 
-def test_tf32x3_mode_plan(kron):
-    # the 3xTF32 mode (dtype code 2) changes only the P = 32 fp32 pairs; fp64 data rejects the mode
-    assert kron.plan_kernels(1024, [32] * 4, [32] * 4, "float32", "3xtf32") == ["kron_fused_tf32x3_kernel"] * 2
-    assert kron.plan_kernels(1024, [8] * 6, [8] * 6, "float32", "3xtf32") == ["kron_fused_pipe_kernel"] * 2
-    assert kron.workspace_size(1024, [32] * 4, [32] * 4, "float32", "3xtf32") == \
-        kron.workspace_size(1024, [32] * 4, [32] * 4, "float32")
-    with pytest.raises(ValueError):
-        kron.dtype_code("float64", "3xtf32")
-    assert _call(kron, 4, [2, 2], [2, 2], dtype=3) == 1   # unknown dtype code
+def test_tensor_core_mode_plans(kron):
+    # the tensor-core modes (dtype codes 2 = 3xTF32, 3 = TF32) route the P = 16 / 32 fp32 square pairs to the
+    # tcgen05 kernel (tc.cu); other passes stay on the fp32 CUDA-core kernels; fp64 data rejects the modes
+    for mode in ("3xtf32", "tf32"):
+        assert kron.plan_kernels(1024, [32] * 4, [32] * 4, "float32", mode) == ["kron_tc_pair_kernel"] * 2
+        assert kron.plan_kernels(1024, [8] * 6, [8] * 6, "float32", mode) == ["kron_fused_pipe_kernel"] * 2
+        # config E: the 16x16 triple stays on the CUDA cores, the pair goes to the tensor cores
+        assert kron.plan_kernels(64, [16] * 5, [16] * 5, "float32", mode) == ["kron_fused_gemm3c_kernel",
+                                                                              "kron_tc_pair_kernel"]
+        assert kron.workspace_size(1024, [32] * 4, [32] * 4, "float32", mode) == \
+            kron.workspace_size(1024, [32] * 4, [32] * 4, "float32")
+        with pytest.raises(ValueError):
+            kron.dtype_code("float64", mode)
+    assert kron.dtype_code("float32", "tf32") == 3 and kron.dtype_code("float32", "3xtf32") == 2
+    assert _call(kron, 4, [2, 2], [2, 2], dtype=4) == 1   # unknown dtype code
 
 
 def test_graph_argument_errors(kron):

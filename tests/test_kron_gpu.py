@@ -187,31 +187,66 @@ def test_autotuned_plan_parity(kron, cuda_device, M, P, Q, dt):
     kron.plan_cache_clear()
 
 
-# ------------------------------------------------------------------ 3xTF32 tensor-core mode (NEXT-4)
+# ------------------------------------------------------------------ tensor-core modes (NEXT-4, tcgen05)
 
-TF32X3 = [
-    (40, [32] * 4, [32] * 4),   # two P = 32 pairs on the tensor cores
-    (9, [32] * 3, [32] * 3),    # pair + single factor (CUDA cores)
+TC = [
+    (40, [32] * 4, [32] * 4),         # two P = 32 pairs on the tcgen05 kernel (2 M-tiles per 8-chunk tile)
+    (9, [32] * 3, [32] * 3),          # pair + single factor (CUDA cores)
     (3, [16, 32, 32], [16, 32, 32]),
+    (5, [16] * 4, [16] * 4),          # P = 16 pairs (64B-swizzled K-major operand, 16-chunk tiles)
+    (3, [16] * 5, [16] * 5),          # config E shape: CUDA-core triple + tensor-core pair
+    (17, [8, 16, 16], [8, 16, 16]),   # rows shorter than a tensor-core tile: CUDA-core fallback
+    (7, [32, 16, 16], [32, 16, 16]),  # pair behind a wider factor, odd M
 ]
+# TF32 mode: positive U[0,1) data, products of operands with 10 explicit mantissa bits (truncated or
+# rounded by the tensor core) through two contractions: relative error <= ~2 * 2 * 2^-10 ~ 4e-3; gate 5e-3
+TF32_TOL = 5e-3
 
 
-@pytest.mark.parametrize("M,P,Q", TF32X3)
-def test_tf32x3_mode_parity(kron, cuda_device, M, P, Q):
-    # small integers are exact in TF32 (lo = 0) and every partial sum is an exact fp32 integer -> bit
-    # exact; U[0,1) data stays within the fp32 bar (the split keeps ~22-bit products)
+@pytest.mark.parametrize("mode", ["3xtf32", "tf32"])
+@pytest.mark.parametrize("M,P,Q", TC)
+def test_tensor_core_mode_parity(kron, cuda_device, M, P, Q, mode):
+    # small integers are exact in TF32 (lo = 0) and every partial sum is an exact fp32 integer -> bit exact in
+    # both modes; U[0,1) data: 3xTF32 within the fp32 bar (~22-bit products), TF32 within TF32_TOL
     import torch
-    for mode, seed_off in (("int1", 11), ("urand", 12)):
-        X, Fs = case(M, P, Q, np.float32, mode, seed_off)
+    for data, seed_off in (("int1", 11), ("urand", 12)):
+        X, Fs = case(M, P, Q, np.float32, data, seed_off)
         ref = oracle.alg1(X, Fs)
-        Y = kron.matmul(to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs], mode="3xtf32")
+        Y = kron.matmul(to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs], mode=mode)
         torch.cuda.synchronize()
         Y = Y.cpu().numpy()
-        if mode == "int1":
+        if data == "int1":
             assert np.array_equal(Y, ref.astype(np.float32))
         else:
-            assert rel_err(Y, ref) <= TOL[np.float32]
-    assert "kron_fused_tf32x3_kernel" in kron.plan_kernels(M, P, Q, "float32", "3xtf32")
+            assert rel_err(Y, ref) <= (TOL[np.float32] if mode == "3xtf32" else TF32_TOL)
+    R = 8 if P[-1] == 32 else 16  # chunks per tensor-core tile
+    if P[-1] in (16, 32) and P[-2] == P[-1] and int(np.prod(P)) % (R * P[-1] ** 2) == 0:
+        assert "kron_tc_pair_kernel" in kron.plan_kernels(M, P, Q, "float32", mode)
+
+
+@pytest.mark.parametrize("M,P,Q", TC[:3])
+def test_tf32x3_mma_sync_fallback(kron, cuda_device, M, P, Q):
+    # round 1's mma.sync 3xTF32 kernel (P = 32 pairs) stays selectable by the autotuner when the tcgen05 kernel
+    # is masked out (KRON_KINDS_MASK without bit 13); fresh process because plans are cached
+    import os
+    import subprocess
+    import sys
+    code = f"""
+import numpy as np, torch, oracle, synth
+from paper_2401_10187_b200 import kron
+M, P, Q = {M}, {P}, {Q}
+X = synth.matrix(M, int(np.prod(P)), synth.SEED_BASE + 12, 0, 'urand', np.float32)
+Fs = synth.factors(P, Q, synth.SEED_BASE + 12, 'urand', np.float32)
+Y = kron.matmul(torch.from_numpy(X).cuda(), [torch.from_numpy(f).cuda() for f in Fs], mode='3xtf32').cpu().numpy()
+ref = oracle.alg1(X, Fs)
+assert float(np.max(np.abs(Y - ref) / np.abs(ref))) <= 1e-5
+assert 'kron_tc_pair_kernel' not in kron.plan_kernels(M, P, Q, 'float32', '3xtf32')
+print('ok', kron.plan_kernels(M, P, Q, 'float32', '3xtf32'))
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, cwd=root,
+                         env={**os.environ, "KRON_KINDS_MASK": "1FFF", "PYTHONPATH": root})
+    assert "ok" in res.stdout, res.stdout + res.stderr
 
 
 @pytest.mark.slow
@@ -222,12 +257,13 @@ def test_tf32x3_full_size_sampled_rows(kron, cuda_device):
     X = torch.empty((M, K), dtype=torch.float32, device=cuda_device)
     synth.fill_device(X.data_ptr(), M, K, seed, 0, "urand", np.float32)
     Fs_h = synth.factors(P, P, seed, "urand", np.float32)
-    Y = kron.matmul(X, [to_dev(f, cuda_device) for f in Fs_h], mode="3xtf32")
     rows = synth.row_subset(M, extra=12)
-    Ys = Y[torch.from_numpy(rows).to(cuda_device)].cpu().numpy()
-    del X, Y
     ref = oracle.alg1(synth.rows_of(rows, K, seed, 0, "urand"), Fs_h)
-    assert rel_err(Ys, ref) <= TOL[np.float32]
+    for mode, tol in (("3xtf32", TOL[np.float32]), ("tf32", TF32_TOL)):
+        Y = kron.matmul(X, [to_dev(f, cuda_device) for f in Fs_h], mode=mode)
+        Ys = Y[torch.from_numpy(rows).to(cuda_device)].cpu().numpy()
+        del Y
+        assert rel_err(Ys, ref) <= tol
 
 
 @pytest.mark.parametrize("M,P,Q,dt", [(20, [2] * 7, [2] * 7, np.float32), (16, [8] * 3, [8] * 3, np.float64),
