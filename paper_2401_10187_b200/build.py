@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libkron.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = ["api.cu", "generic.cu", "fused.cu", "gemm.cu", "dist.cu", "tc.cu"]
+SOURCES = ["api.cu", "generic.cu", "fused.cu", "gemm.cu", "dist.cu", "tc.cu", "chain.cu"]
 NVCC = os.environ.get("NVCC", "nvcc")
 def _nccl_include() -> str:
     try:

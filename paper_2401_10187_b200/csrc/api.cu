@@ -195,6 +195,10 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
       for (int k = 0; k < pp.nf; ++k) grp[k] = F[pp.first - 1 - k];
       err = launch_fused(pp, plan.dtype, plan.M, in, out, grp, stream, lastp ? push : nullptr,
                          firstp ? rin : nullptr);
+    } else if (pp.kind == KIND_CHAIN) {
+      const void *grp[kMaxFused];
+      for (int k = 0; k < pp.nf; ++k) grp[k] = F[pp.first - 1 - k];
+      err = launch_chain(pp, plan.dtype, plan.M, in, out, grp, stream);
     } else if (pp.kind == KIND_GEMM) {
       err = launch_gemm(pp, plan.dtype, plan.M, in, out, F[pp.first - 1], stream);
     } else {
@@ -202,6 +206,7 @@ kron_status_t run_plan(const Plan &plan, const void *X, const void *const *F, vo
     }
     if (err != 0)
       return cuda_fail(err, pp.kind == KIND_FUSED ? "fused pass launch"
+                            : pp.kind == KIND_CHAIN ? "chain pass launch"
                             : pp.kind == KIND_GEMM ? "gemm pass launch" : "generic pass launch");
   }
   if (events && cudaEventRecord((cudaEvent_t)events[ip], (cudaStream_t)stream) != cudaSuccess) return KRON_ERR_CUDA;
@@ -399,6 +404,47 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
           f -= k;
         }
         continue;
+      }
+    }
+    // any square P (odd sizes, rows a TMA map cannot describe): fused chain passes without TMA (chain.cu)
+    if (p == q && p <= 16 && allowed(14)) {
+      int run = 1;
+      while (f - run >= 1 && P[f - run - 1] == p && Q[f - run - 1] == p && run < 64) ++run;
+      int kmax = 0;
+      PassPlan probe;
+      for (int k = 2; k <= run && k <= kMaxFused && k <= policy.kcap; ++k)
+        if (chain_geometry(p, k, dtype, W, policy.chain_rdiv, &probe)) kmax = k;
+      if (kmax >= 2) {
+        // fewest passes, then balanced group sizes; any size the balanced split cannot tile falls back
+        // to kmax-sized groups
+        const int npass = (run + kmax - 1) / kmax;
+        const int base = run / npass, extra = run % npass;
+        bool ok = true;
+        std::vector<int> sizes;
+        for (int i = 0; i < npass; ++i) {
+          const int k = base + (i < extra ? 1 : 0);
+          ok &= k == 1 || chain_geometry(p, k, dtype, W, policy.chain_rdiv, &probe);
+          sizes.push_back(k);
+        }
+        if (!ok) {
+          sizes.clear();
+          for (int left = run; left > 0; left -= kmax) sizes.push_back(left < kmax ? left : kmax);
+        }
+        int done = 0;
+        for (int k : sizes) {
+          PassPlan cp;
+          if (k >= 2 && chain_geometry(p, k, dtype, W, policy.chain_rdiv, &cp)) {
+            cp.first = f;
+            cp.W_in = W;
+            cp.W_out = W;
+            plan->passes.push_back(cp);
+            f -= k;
+            done += k;
+          } else {
+            break;  // the rest goes through the single-factor passes below
+          }
+        }
+        if (done > 0) continue;
       }
     }
     PassPlan pp;
@@ -701,7 +747,7 @@ kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x3FFFu;
+  const unsigned all = 0x7FFFu;
   const unsigned v10 = (1u << 11) | (1u << 12);  // constant-bank kernels vs their round-1 shared-memory twins
   const unsigned kinds[] = {all, all & ~v10, all & ~(1u << 12), all & ~(1u << 11), all & ~((1u << 10) | (1u << 12)),
                             all & ~(1u << 13), all & ~((1u << 13) | v10), all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
@@ -713,11 +759,13 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
     for (size_t i = 0; i < a.passes.size(); ++i) {
       const PassPlan &x = a.passes[i], &y = b.passes[i];
       if (x.kind != y.kind || x.variant != y.variant || x.first != y.first || x.nf != y.nf || x.tileK != y.tileK ||
+          x.R != y.R ||
           x.tileM != y.tileM || x.stages != y.stages)
         return false;
     }
     return true;
   };
+  for (int rd : {1, 2, 4})
   for (int st = 0; st <= 1; ++st)
   for (int dm = 1; dm >= 0; --dm)
     for (unsigned km : kinds)
@@ -727,6 +775,7 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
         pol.kinds = km;
         pol.dmma = dm == 1;
         pol.short_tiles = st == 1;
+        pol.chain_rdiv = rd;
         Plan pl;
         if (make_plan(M, N, P, Q, dtype, &pl, 1, pol) != KRON_OK) continue;
         bool dup = false;
@@ -835,7 +884,9 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
   if (pass < 0 || pass >= (int32_t)pl->passes.size()) return KRON_ERR_INVALID_ARG;
   const PassPlan &pp = pl->passes[pass];
   const char *k = "sliced_generic_kernel";
-  if (pp.kind == KIND_GEMM) {
+  if (pp.kind == KIND_CHAIN) {
+    k = "kron_chain_kernel";
+  } else if (pp.kind == KIND_GEMM) {
     k = pp.variant == 1 ? "kron_dmma_kernel" : "kron_gemm_kernel";
   } else if (pp.kind == KIND_FUSED) {
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",

@@ -10,7 +10,7 @@
 
 namespace kron {
 
-enum Kind { KIND_GENERIC = 0, KIND_FUSED = 1, KIND_GEMM = 2 };
+enum Kind { KIND_GENERIC = 0, KIND_FUSED = 1, KIND_GEMM = 2, KIND_CHAIN = 3 };
 enum Buf { BUF_X = 0, BUF_Y = 1, BUF_WS0 = 2, BUF_WS1 = 3 };
 
 constexpr int kMaxFactors = 64;
@@ -48,11 +48,13 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0x3FFFu;    // allowed fused kernel families (bit = FusedInstance::warp)
+  unsigned kinds = 0x7FFFu;    // allowed fused kernel families (bit = FusedInstance::warp; bit 14 = chain.cu)
+  int chain_rdiv = 1;         // chain passes: tile of R / chain_rdiv chunks (autotuner tile-size candidates)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
   bool operator==(const PlanPolicy &o) const {
-    return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma && short_tiles == o.short_tiles;
+    return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma && short_tiles == o.short_tiles &&
+           chain_rdiv == o.chain_rdiv;
   }
 };
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
@@ -109,6 +111,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 // input-box geometry of a fused pass (lines of 128 bytes per TMA box); shared by launch_fused and plan_remap_ok
 int fused_box_lines(const PassPlan &pp, int dtype);
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream);
+// fused passes of any square P without TMA (chain.cu, NEXT-3)
+bool chain_geometry(int P, int k, int dtype, int64_t W, int rdiv, PassPlan *pp);
+int launch_chain(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *const *Fgroup,
+                 void *stream);
 // tcgen05 fp32 pair (tc.cu, NEXT-4): geometry for P = 16 / 32 pairs in mode 1 (TF32) / 2 (3xTF32), and launch
 bool tc_geometry(int P, int mode, int64_t W, PassPlan *pp);
 int launch_tc(const PassPlan &pp, int64_t M, const void *in, void *out, const void *const *Fgroup, void *stream);

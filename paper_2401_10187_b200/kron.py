@@ -73,7 +73,7 @@ _lib.kron_matmul_host.restype = ctypes.c_int
 _lib.kron_matmul_host.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_void_p, _vpp, ctypes.c_void_p,
                                   ctypes.c_int, ctypes.c_int64, ctypes.c_void_p]
 
-KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm"}
+KIND_NAMES = {0: "generic", 1: "fused", 2: "gemm", 3: "chain"}
 
 
 class KronError(RuntimeError):

@@ -72,7 +72,8 @@ def test_plan_configs(kron):
     assert kron.plan_describe(1024, [32] * 4, [32] * 4, f32) == [(4, 2, "fused"), (2, 2, "fused")]
     assert kron.plan_describe(1024, [32] * 4, [32] * 4, f64) == [(4, 2, "fused"), (2, 2, "fused")]
     # config A: K = 16 is narrower than one 128-byte TMA line -> generic
-    assert [k for _, _, k in kron.plan_describe(16, [4, 4], [4, 4], f32)] == ["generic", "generic"]
+    # config A: rows of 16 are too short for the TMA kernels; both factors fuse in one chain pass (chain.cu)
+    assert kron.plan_describe(16, [4, 4], [4, 4], f32) == [(2, 2, "chain")]
     # every plan applies every factor exactly once, N -> 1
     for P, Q, dt in [([16] * 5, [16] * 5, f32), ([128] * 3, [128] * 3, f64), ([64] * 3, [32] * 3, f64),
                      ([3, 8, 8, 8, 5], [4, 8, 8, 8, 2], f32), ([2] * 12, [2] * 12, f64)]:
@@ -145,7 +146,7 @@ def test_autotune_candidates(kron):
     # the autotuner times alternative plans; the static plan is always one of them
     assert kron.autotune_candidates(1024, [8] * 6, [8] * 6, "float32") >= 3   # fusion caps 3/2/1 + families
     assert kron.autotune_candidates(1024, [32] * 4, [32] * 4, "float64") >= 2  # + DMMA on/off
-    assert kron.autotune_candidates(16, [4, 4], [4, 4], "float32") == 1       # generic only
+    assert kron.autotune_candidates(16, [4, 4], [4, 4], "float32") == 2       # one chain pass or two generic
     assert kron.autotune_candidates(0, [8] * 2, [8] * 2, "float32") == 0
     lib = kron.raw_lib()
     Pa = (ctypes.c_int32 * 2)(2, 2)
@@ -158,7 +159,7 @@ def test_plan_kernels(kron):
     assert kron.plan_kernels(1024, [8] * 6, [8] * 6, "float32") == ["kron_fused_pipe_kernel"] * 2
     assert kron.plan_kernels(1024, [32] * 4, [32] * 4, "float64") == ["kron_fused_dmma2_kernel"] * 2
     assert kron.plan_kernels(320, [128] * 3, [128] * 3, "float64") == ["kron_dmma_kernel"] * 3
-    assert kron.plan_kernels(16, [4, 4], [4, 4], "float32") == ["sliced_generic_kernel"] * 2
+    assert kron.plan_kernels(16, [4, 4], [4, 4], "float32") == ["kron_chain_kernel"]
     lib = kron.raw_lib()
     Pa = (ctypes.c_int32 * 2)(4, 4)
     buf = ctypes.create_string_buffer(8)
@@ -235,3 +236,13 @@ def test_dist_round_info_fused_layouts(kron):
         kron.DistContext("virtual", GM=1, GK=2, chunks=0)
     for c in (ctx, ctx2, ctx3):
         c.close()
+
+
+def test_chain_plans_for_odd_p(kron):
+    # square factors of any size P fuse through chain.cu (Fused <= floor(log_P TileK)): the paper's Table 4
+    # shapes 3^7 (one pass of 7) and 6^7 (4 + 3); power-of-2 P keeps the TMA kernels
+    assert kron.plan_describe(1024, [3] * 7, [3] * 7, "float32") == [(7, 7, "chain")]
+    assert kron.plan_describe(1024, [6] * 7, [6] * 7, "float32") == [(7, 4, "chain"), (3, 3, "chain")]
+    assert kron.plan_kernels(1024, [4] * 7, [4] * 7, "float32") == ["kron_fused_warp_kernel", "kron_fused_pipe_kernel"]
+    # the autotuner searches the chain tile size (R / 1, 2, 4 chunks per tile) besides the plan families
+    assert kron.autotune_candidates(1024, [6] * 7, [6] * 7, "float32") >= 3

@@ -187,6 +187,35 @@ def test_autotuned_plan_parity(kron, cuda_device, M, P, Q, dt):
     kron.plan_cache_clear()
 
 
+# ------------------------------------------------------------------ fused chains of any square P (NEXT-3)
+
+CHAIN = [
+    (9, [3] * 7, [3] * 7),            # Table 4 #17 shape (3^7): one pass of seven fused factors, whole-row tile
+    (5, [6] * 7, [6] * 7),            # Table 4 #19 shape (6^7): passes of 4 + 3 fused factors (even chunk, padded)
+    (3, [5] * 4, [5] * 4),
+    (4, [7] * 3 + [2], [7] * 3 + [2]),  # chain behind a single 2x2 factor
+    (6, [12] * 3, [12] * 3),
+    (2, [2] * 3 + [3] * 4, [2] * 3 + [3] * 4),  # mixed runs: fused power-of-2 and chain passes
+]
+
+
+@pytest.mark.parametrize("M,P,Q", CHAIN)
+def test_chain_parity(kron, cuda_device, M, P, Q):
+    import torch
+    assert "kron_chain_kernel" in kron.plan_kernels(M, P, Q, "float32")
+    for dt, data, seed_off in ((np.float32, "int1", 21), (np.float32, "urand", 22), (np.float64, "int", 23),
+                               (np.float64, "urand", 24)):
+        X, Fs = case(M, P, Q, dt, data, seed_off)
+        ref = oracle.alg1(X, Fs)
+        Y = kron.matmul(to_dev(X, cuda_device), [to_dev(f, cuda_device) for f in Fs])
+        torch.cuda.synchronize()
+        Y = Y.cpu().numpy()
+        if data.startswith("int"):
+            assert np.array_equal(Y, ref.astype(dt))
+        else:
+            assert rel_err(Y, ref) <= TOL[dt]
+
+
 # ------------------------------------------------------------------ tensor-core modes (NEXT-4, tcgen05)
 
 TC = [
