@@ -561,7 +561,7 @@ def run_dist(args, kron, synth, torch, ws, rank, local, dev, barrier):
     cfg, M, P, Q, dtn = CONFIGS[cfg_name]
     weak = cfg_name in WEAK
     if weak:
-        M = M * ws
+        M = (args.rows or M) * ws  # rows per GPU x GPUs (Fig 11: memory per GPU constant)
     dt = np.float32 if dtn == "float32" else np.float64
     tdt = torch.float32 if dt == np.float32 else torch.float64
     es = 4 if dt == np.float32 else 8
@@ -695,6 +695,8 @@ def main():
                          "kernels over peer memory (NEXT-1, P:652)")
     ap.add_argument("--grid", default=None, help="GMxGK for the distributed path (default: the paper rule)")
     ap.add_argument("--chunks", type=int, default=2, help="row chunks per round (exchange / compute overlap)")
+    ap.add_argument("--rows", type=int, default=None,
+                    help="W64 / W128: rows per GPU (default: the Fig 11 sizes, 16 GiB of X per GPU)")
     ap.add_argument("--mode", default=None, choices=["3xtf32", "tf32"],
                     help="fp32 configs only: the separately reported tcgen05 tensor-core modes (NEXT-4)")
     ap.add_argument("--autotune", action=argparse.BooleanOptionalAction, default=True,

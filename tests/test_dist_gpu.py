@@ -37,6 +37,7 @@ GRIDS = [
     (1, 2, 3, [2, 16, 16, 16, 8, 8], [2, 16, 16, 16, 8, 8]),  # v9 ends a round with rho = 1 (no float4 push)
     (1, 2, 3, [2, 16, 16, 8, 8, 4, 4], [2, 16, 16, 8, 8, 4, 4]),  # 3-pass round ending in a v6 pair
     (1, 2, 5, [32] * 4, [32] * 4),    # C32 shapes: v6 P = 32 pairs with the fused send / receive layout
+    (2, 2, 2, [64] * 4, [64] * 4),    # Fig 11 weak-scaling workload shape (P = 64, N = 4), K = 2^24
 ]
 # (chunks, fused): the default (2 row chunks, fused layouts), the unfused kernels, ragged chunks
 MODES = [(2, True), (1, False), (3, True)]
