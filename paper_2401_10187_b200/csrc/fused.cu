@@ -1830,6 +1830,16 @@ __device__ __forceinline__ uint32_t rowswz32(uint32_t r, uint32_t c) {  // [rows
   const uint32_t line = 2u * r + (c >> 4);
   return line * 128u + (((c & 15u) << 3) ^ ((line & 7u) << 4));
 }
+// The same [rows][32 doubles] rows with the 16-byte granule XOR'd by (r & 1) * 4 + ((r >> 1) & 1) * 2 instead of
+// the TMA line pattern: with it the accumulator write-back (STS.128, lanes = 8 rows x 4 column pairs), the
+// B-fragment gathers (LDS.64, 4 rows x 8 columns) and the chunk-fastest stream-out reads are all at ncu's ideal
+// wavefront count (a GF(2) search with a bank model, tools/swizzle_search.py; with the TMA pattern the
+// write-back took 2x its ideal wavefronts: profiles/r02_banks_C64.json).  Used for Z and OUT, which the kernel
+// itself writes; X keeps the TMA layout (rowswz32).
+__device__ __forceinline__ uint32_t rowswzZ(uint32_t r, uint32_t c) {
+  const uint32_t line = 2u * r + (c >> 4);
+  return line * 128u + (((c & 15u) << 3) ^ ((((r & 1u) << 2) | (r & 2u)) << 4));
+}
 
 // Warp-specialised: NCW compute warps (one chunk each per tile; with NCW = 2 * CPT two groups take
 // alternate tiles; NCW = 8 gives every SM sub-partition two DMMA warps) never stop for the HBM stream-out, which NSW
@@ -1923,7 +1933,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int v1 = 0; v1 < 2; ++v1)
-            *reinterpret_cast<double2 *>(cb0 + rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+            *reinterpret_cast<double2 *>(cb0 + rowswzZ(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
                 make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
       __syncwarp();
       // ---- GEMM2: OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
@@ -1942,7 +1952,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
           a1[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq + 8, k0 + tq));
         }
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswz32(k0 + tq, nt * 8 + gq));
+        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswzZ(k0 + tq, nt * 8 + gq));
 #pragma unroll
         for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
@@ -1955,7 +1965,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int v1 = 0; v1 < 2; ++v1)
-            *reinterpret_cast<double2 *>(cb0 + (rowswz32(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
+            *reinterpret_cast<double2 *>(cb0 + (rowswzZ(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
                 make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
       __syncwarp();
       mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
@@ -1980,7 +1990,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
 #pragma unroll 4
         for (int w = sw; w < C / UPW; w += NSW) {
           const int u = w * UPW + lane / CPT;
-          const double v = *reinterpret_cast<const double *>(buf + (rowswz32((uint32_t)u / P, (uint32_t)u % P) ^ gx));
+          const double v = *reinterpret_cast<const double *>(buf + (rowswzZ((uint32_t)u / P, (uint32_t)u % P) ^ gx));
           yg[(int64_t)u * a.WC] = v;
         }
       }
@@ -2106,7 +2116,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
         for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
           for (int v1 = 0; v1 < 2; ++v1)
-            *reinterpret_cast<double2 *>(cb0 + rowswz32(h * 32 + mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+            *reinterpret_cast<double2 *>(cb0 + rowswzZ(h * 32 + mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
                 make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
       named_bar_sync(2 + pair, 64);  // both halves of Z written (and both GEMM1s done with the p >= 32 half)
       // ---- GEMM2 (rows q2 = 16h..16h+15): OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
@@ -2122,17 +2132,17 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
         const double a1 = *reinterpret_cast<const double *>(F2Ts + rowswz64(r + 8, k0 + tq));
         double b[4];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswz32(k0 + tq, nt * 8 + gq));
+        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswzZ(k0 + tq, nt * 8 + gq));
 #pragma unroll
         for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc2[nt], a0, a1, b[nt]);
       }
-      // OUT rows into the p >= 32 half (no longer read by anyone); [32][32], rowswz32
+      // OUT rows into the p >= 32 half (no longer read by anyone); [32][32], rowswzZ
       unsigned char *ob = cb0 + HB;
 #pragma unroll
       for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
         for (int v1 = 0; v1 < 2; ++v1)
-          *reinterpret_cast<double2 *>(ob + rowswz32(h * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+          *reinterpret_cast<double2 *>(ob + rowswzZ(h * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
               make_double2(acc2[nt][2 * v1], acc2[nt][2 * v1 + 1]);
       __syncwarp();
       mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
@@ -2151,7 +2161,7 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2g_kernel(
       double *yg = Y + (int64_t)rb * a.Wout + g;
 #pragma unroll 4
       for (int u = sw * 32 + lane; u < CO; u += NSW * 32)
-        yg[(int64_t)u * a.WC] = *reinterpret_cast<const double *>(ob + rowswz32((uint32_t)u / Q, (uint32_t)u % Q));
+        yg[(int64_t)u * a.WC] = *reinterpret_cast<const double *>(ob + rowswzZ((uint32_t)u / Q, (uint32_t)u % Q));
       __syncwarp();
       mbar_arrive(&empty[st]);
       if (sw == 0) {

@@ -291,7 +291,7 @@ __global__ void __launch_bounds__((NWARP + 1 + NSW) * 32, 1) kron_dmma_kernel(co
         for (int q = sw; q < BN; q += NSW) {
           const int qg = ntile * BN + q;
           if (qg >= g.Q) break;
-          const double2 v = *reinterpret_cast<const double2 *>(stg + (size_t)q * BM + rb + 2 * lane);
+          const double2 v = *reinterpret_cast<const double2 *>(stg + (size_t)q * BM + ((rb + 2 * lane) ^ (4 * ((q >> 1) & 3))));
           if (pair) {
             *reinterpret_cast<double2 *>(Y + m0 * g.Wout + (int64_t)qg * g.S + s0) = v;
           } else {
@@ -376,7 +376,10 @@ __global__ void __launch_bounds__((NWARP + 1 + NSW) * 32, 1) kron_dmma_kernel(co
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int row = wm * WTM + mt * 16 + gq + 8 * (e >> 1), col = wn * 32 + nt * 8 + 2 * tq + (e & 1);
-            stg[(size_t)col * BM + row] = acc[mt][nt][e];
+            // rows XOR 4*((col/2) % 4): the four tq lanes of an accumulator column pair land in four different
+            // 8-row bank groups (unswizzled, the 1 KB column stride put them on the same banks: ncu counted
+            // 8 wavefronts per STS.64 against 2 ideal, profiles/r02_banks_D1.json); row pairs stay adjacent
+            stg[(size_t)col * BM + (row ^ (4 * ((col >> 1) & 3)))] = acc[mt][nt][e];
             acc[mt][nt][e] = 0.0;
           }
       mbar_arrive(sfull);
