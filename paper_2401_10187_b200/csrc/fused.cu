@@ -2020,7 +2020,9 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
 // chunk to Y[row][u*(W/C) + g]; a CTA walks a contiguous range of chunks so consecutive chunks' stores
 // land next to each other while their L2 lines are still resident.
 __device__ __forceinline__ uint32_t rowswz64(uint32_t r, uint32_t c) {  // [rows][64 doubles], thread-filled
-  return r * 512u + ((c * 8u) ^ ((r & 7u) << 4));
+  // granule XOR 2*(r % 4) + (r / 4) % 2: the A-fragment gathers (4 rows x 4 consecutive doubles per half-warp)
+  // hit 8 distinct granules (with r % 8 they paired up: 2x the ideal wavefronts, profiles/r02_banks_D2.json)
+  return r * 512u + ((c * 8u) ^ ((((r & 3u) << 1) | ((r >> 2) & 1u)) << 4));
 }
 
 template <int NCW, int NSW>

@@ -78,3 +78,13 @@ def hz(r, chi): return ((r & 1) << 2) | (((r >> 1) & 1) << 1)
 print('p4 current', p4(cur), 'p4 new', p4(make_off(hz)))
 res = patterns(make_off(hz))
 for p in ('p1', 'p2', 'p3'): print('new', p, score(res, (p,)))
+
+# v7: F2^T tile [32 rows][64 doubles] (512-byte rows), A-fragment gathers r = R0 + gq, c = k0 + tq (LDS.64)
+def f2t_cost(h):
+    tot = idl = 0
+    for R0 in (0, 8, 16, 24):
+        for k0 in range(0, 64, 4):
+            a = [(R0 + l // 4) * 512 + (((k0 + l % 4) * 8) ^ (h(R0 + l // 4) << 4)) for l in range(32)]
+            tot += wavefronts(a, 8); idl += ideal(a, 8)
+    return tot, idl
+print('F2T rowswz64', f2t_cost(lambda r: r & 7), 'new', f2t_cost(lambda r: ((r & 3) << 1) | ((r >> 2) & 1)))
