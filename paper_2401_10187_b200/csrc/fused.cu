@@ -576,6 +576,16 @@ __device__ __forceinline__ uint32_t pipe_gx(uint32_t chunk) {
   else return (g2 | (g1 << 1) | ((g0 ^ g2) << 2)) << 4;
 }
 
+// v3's chunk granule XOR: the last group's loads of one instruction cover chunks j*VS + i (j = 0..7 across a
+// quarter-warp, i fixed), so the XOR must be injective on chunk / VS — round 1's 3x3 map over the chunk's low
+// bits gave only four distinct values on even chunks (VS = 2: ncu counted 2x the ideal wavefronts on those
+// LDS.128, profiles/r02_banks_B.json).  The middle groups' stores XOR a warp-constant value (one chunk per warp
+// region), so any injective map keeps them conflict-free.
+template <int VS>
+__device__ __forceinline__ uint32_t pipe3_gx(uint32_t chunk) {
+  return ((chunk / VS) & 7u) << 4;
+}
+
 template <typename T, int N>
 struct VecIO;
 template <>
@@ -699,7 +709,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
       for (uint32_t grp = (uint32_t)wg; grp < nreg; grp += NWG) {
         unsigned char *gb = buf + grp * (GE * ES);
         const uint32_t chunk = grp * (GE / C) + cl;
-        const uint32_t gx = gx_on ? pipe_gx<P, ES>(chunk) : 0u;
+        const uint32_t gx = gx_on ? pipe3_gx<VS>(chunk) : 0u;
         const uint32_t gxr = g == 0 ? 0u : gx;  // step 0 reads the plain TMA layout
         T x[VS][P];
 #pragma unroll
@@ -775,7 +785,7 @@ __device__ __forceinline__ void pipe_group(const FusedArgs &a, const CUtensorMap
 #pragma unroll
       for (int i = 0; i < VS; ++i) {
         const uint32_t chunk = sl_chunk[k] + i;
-        const uint32_t gx = (chained && gx_on) ? pipe_gx<P, ES>(chunk) : 0u;
+        const uint32_t gx = (chained && gx_on) ? pipe3_gx<VS>(chunk) : 0u;
         T x[P];
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
