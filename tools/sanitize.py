@@ -28,18 +28,28 @@ CASES = [
     (2, [128, 128], [128, 128], np.float64),    # DMMA gemm (128-column tiles)
     (2, [64, 64], [64, 64], np.float32),        # FFMA2 gemm
     (3, [3, 5], [4, 2], np.float32),            # generic
+    # round 2
+    (3, [8, 16, 16, 16], [8, 16, 16, 16], np.float32, None),    # v10 triple (constant-bank FFMA2, groups of 4)
+    (2, [16] * 4, [16] * 4, np.float32, None),                  # v10 pair
+    (3, [3] * 5, [3] * 5, np.float32, None),                    # chain (odd P, one pass)
+    (2, [6] * 5, [6] * 5, np.float64, None),                    # chain (even chunk, padded, cp.async 16 B)
+    (17, [32] * 3, [32] * 3, np.float32, "tf32"),               # tcgen05 pair, TF32
+    (17, [32] * 3, [32] * 3, np.float32, "3xtf32"),             # tcgen05 pair, 3xTF32
+    (5, [32, 16, 16], [32, 16, 16], np.float32, "3xtf32"),      # tcgen05 pair, P = 16
 ]
 
 
 def main():
     dev = torch.device("cuda:0")
-    for M, P, Q, dt in CASES:
+    for case in CASES:
+        M, P, Q, dt = case[:4]
+        mode = case[4] if len(case) > 4 else None
         seed = synth.SEED_BASE + 77
         X = synth.matrix(M, int(np.prod(P)), seed, 0, "urand", dt)
         Fs = synth.factors(P, Q, seed, "urand", dt)
-        Y = kron.matmul(torch.from_numpy(X).to(dev), [torch.from_numpy(f).to(dev) for f in Fs])
+        Y = kron.matmul(torch.from_numpy(X).to(dev), [torch.from_numpy(f).to(dev) for f in Fs], mode=mode)
         torch.cuda.synchronize()
-        print("ok", M, P, Q, np.dtype(dt).name, kron.plan_kernels(M, P, Q, np.dtype(dt).name), float(Y.sum()))
+        print("ok", M, P, Q, np.dtype(dt).name, mode, kron.plan_kernels(M, P, Q, np.dtype(dt).name, mode), float(Y.sum()))
     # the autotuner runs every candidate plan of one shape
     X = torch.from_numpy(synth.matrix(2, 16 ** 4, 5, 0, "urand", np.float32)).to(dev)
     _, n, _ = kron.autotune(X, [torch.from_numpy(f).to(dev) for f in synth.factors([16] * 4, [16] * 4, 5, "urand", np.float32)], reps=1)
@@ -52,7 +62,7 @@ def main():
     Fs = [torch.from_numpy(f).to(dev) for f in synth.factors([16] * 3, [16] * 3, 1, "urand", np.float32)]
     kron.matmul_dist(4, blocks, Fs, ctx)
     torch.cuda.synchronize()
-    print("ok dist virtual 2x2")
+    print("ok dist virtual 2x2 (fused send / receive layouts, 2 row chunks)", ctx.round_info(4, [16] * 3, [16] * 3, "float32"))
 
 
 if __name__ == "__main__":
