@@ -458,6 +458,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     pp.W_out = plan->W[f - 1];
     pp.kind = gemm_supported(dtype, Mp, W, p, q) ? KIND_GEMM : KIND_GENERIC;
     pp.variant = (pp.kind == KIND_GEMM && dtype == KRON_F64 && policy.dmma && p % 16 == 0 && q % 16 == 0) ? 1 : 0;
+    if (pp.kind == KIND_GEMM && dtype == KRON_F32 && allowed(15) && sgemm_supported(Mp, W, p, q)) pp.variant = 2;
     plan->passes.push_back(pp);
     f -= 1;
   }
@@ -747,7 +748,7 @@ kron_status_t kron_matmul_host(int64_t M, int32_t N, const int32_t *P, const int
 // duplicates removed; the static plan (no cap, all families, DMMA) is always candidate 0.
 std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype) {
   // candidate policies: fusion-depth caps x kernel families x DMMA; duplicate plans removed
-  const unsigned all = 0x7FFFu;
+  const unsigned all = 0xFFFFu;
   const unsigned v10 = (1u << 11) | (1u << 12);  // constant-bank kernels vs their round-1 shared-memory twins
   const unsigned kinds[] = {all, all & ~v10, all & ~(1u << 12), all & ~(1u << 11), all & ~((1u << 10) | (1u << 12)),
                             all & ~(1u << 13), all & ~((1u << 13) | v10), all & ~(1u << 2), all & ~((1u << 5) | (1u << 6) | (1u << 7)),
@@ -887,7 +888,7 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
   if (pp.kind == KIND_CHAIN) {
     k = "kron_chain_kernel";
   } else if (pp.kind == KIND_GEMM) {
-    k = pp.variant == 1 ? "kron_dmma_kernel" : "kron_gemm_kernel";
+    k = pp.variant == 1 ? "kron_dmma_kernel" : pp.variant == 2 ? "kron_sgemm_kernel" : "kron_gemm_kernel";
   } else if (pp.kind == KIND_FUSED) {
     static const char *names[] = {"kron_fused_kernel",       "kron_fused_warp_kernel",  "kron_fused_pipe_kernel",
                                   "kron_fused_gemm2_kernel", "kron_fused_pipe_kernel",  "kron_fused_dmma2_kernel",

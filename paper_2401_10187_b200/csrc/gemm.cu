@@ -170,6 +170,198 @@ __global__ void __launch_bounds__(256, 1) kron_gemm_kernel(const __grid_constant
   }
 }
 
+// ------------------------------------------------------------------ fp32 large-P pass, round 2 (sgemm)
+//
+// The fp32 GEMM above (TN = 4 columns per thread read as scalar LDS with stride GN) issues 24 shared loads per
+// 64 FFMA2 and reached 0.34 (P = 64) / 0.54 (P = 128) of the FP32 peak on the Fig 11 workloads.  This kernel
+// reorganises the thread tile around FFMA2's broadcast operand form `FFMA2 acc(q,q+1), x.F32, F(q,q+1).F32x2`:
+//   * every lane of a warp shares the warp's QT-column range [q0, q0+QT) and owns RS = 8 slices
+//     s = sg*256 + lane + 32*i, so a factor row segment F[p][q0..q0+QT) is one broadcast LDS.128 per 4 columns
+//     (1 wavefront) and feeds 8 slices;
+//   * the slices' elements come from the TMA-staged [slice][32 p] 128-byte lines (128B swizzle: lanes 0-7 of a
+//     phase hit 8 distinct 16-byte chunks), one LDS.128 per 4 p per slice;
+//   -> per 4 p: 8 + QT/4*4 shared loads for 4*8*QT/2 FFMA2 (QT = 16: 24 loads per 256 FFMA2);
+//   * F (padded to whole 32-p chunks, zero rows) stays resident in shared memory for the CTA's life;
+//   * the epilogue stores from registers: for a fixed (slice i, column q) the warp's 32 lanes hold 32
+//     consecutive slices, i.e. 128 contiguous bytes of Y[m, q*S + s] (the direct-index store).
+// CTA = 8 warps = QR column ranges x SG = 8/QR slice groups; a tile is SG*256 slices x QR*QT columns.
+struct SgemmArgs {
+  int64_t ntiles;
+  int rows;   // M * S  (< 2^31: TMA coordinates)
+  int S;      // slices per row of T
+  int P, Q;
+  int64_t Wout;
+  int nk;     // 32-p chunks
+};
+
+__device__ __forceinline__ void st_global_f32(float *p, float v) { asm("st.global.f32 [%0], %1;" ::"l"(p), "f"(v)); }
+
+template <int QT, int QR, int SG, int RS, int NS>
+__global__ void __launch_bounds__(QR *SG * 32, 1) kron_sgemm_kernel(const __grid_constant__ CUtensorMap tm_a,
+                                                                  const float *__restrict__ F, float *__restrict__ Y,
+                                                                  const SgemmArgs g) {
+  constexpr int NT = QR * SG * 32, SL = SG * 32 * RS, QTILE = QT * QR, QP = QT / 2;
+  static_assert(SL % 256 == 0, "whole 256-row TMA boxes");
+  constexpr uint32_t STAGE = SL * 128u;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  float *Fs = reinterpret_cast<float *>(base + NS * STAGE);  // [nk*32][QTILE]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(Fs + g.nk * 32 * QTILE);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int qr = warp % QR, sg = warp / QR, q0 = qr * QT;
+
+  for (int i = tid; i < g.nk * 32 * QTILE; i += NT) {
+    const int p = i / QTILE, q = i - p * QTILE;
+    Fs[i] = (p < g.P && q < g.Q) ? F[(int64_t)p * g.Q + q] : 0.f;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+    prefetch_tmap(&tm_a);
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t z) {
+    const int64_t t = z / g.nk;
+    const int k = (int)(z - t * g.nk);
+    const int64_t tile = blockIdx.x + t * gridDim.x;
+    if (tile >= g.ntiles) return;
+    const int st = (int)(z % NS);
+    unsigned char *sa = base + st * STAGE;
+    mbar_arrive_expect_tx(&bars[st], STAGE);
+#pragma unroll
+    for (int b = 0; b < SL / 256; ++b) tma_load_2d(sa + b * 256 * 128, &tm_a, &bars[st], k * 32, (int)(tile * SL) + b * 256);
+  };
+  if (tid == 0)
+    for (int z = 0; z < NS; ++z) issue(z);
+
+  float2 acc[RS][QP];
+#pragma unroll
+  for (int i = 0; i < RS; ++i)
+#pragma unroll
+    for (int j = 0; j < QP; ++j) acc[i][j] = make_float2(0.f, 0.f);
+
+  const bool active = q0 < g.Q;
+  const uint32_t xsw = (uint32_t)(lane & 7) << 4;  // 128B swizzle of the lane's slice rows (sg*256 + 32i = 0 mod 8)
+  for (int64_t z = 0;; ++z) {
+    const int64_t t = z / g.nk;
+    const int k = (int)(z - t * g.nk);
+    const int64_t tile = blockIdx.x + t * gridDim.x;
+    if (tile >= g.ntiles) break;
+    const int st = (int)(z % NS);
+    mbar_wait(&bars[st], (uint32_t)((z / NS) & 1));
+    if (active) {
+      const unsigned char *xs = base + st * STAGE + (size_t)(sg * 32 * RS + lane) * 128;
+      const float *fk = Fs + (k * 32) * QTILE + q0;
+#pragma unroll 2
+      for (int pc = 0; pc < 8; ++pc) {
+        float4 xv[RS];
+#pragma unroll
+        for (int i = 0; i < RS; ++i)
+          xv[i] = *reinterpret_cast<const float4 *>(xs + i * 32 * 128 + (((uint32_t)pc << 4) ^ xsw));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float4 fv[QT / 4];
+#pragma unroll
+          for (int j = 0; j < QT / 4; ++j) fv[j] = *reinterpret_cast<const float4 *>(fk + (pc * 4 + e) * QTILE + 4 * j);
+          // factor pair outer: consecutive FFMA2s share the F pair operand (W64 47.0 -> 45.7 ms against the
+          // slice-outer order)
+#pragma unroll
+          for (int j = 0; j < QP; ++j) {
+            const float2 ff = (j & 1) ? make_float2(fv[j >> 1].z, fv[j >> 1].w) : make_float2(fv[j >> 1].x, fv[j >> 1].y);
+#pragma unroll
+            for (int i = 0; i < RS; ++i) {
+              const float xe = e == 0 ? xv[i].x : e == 1 ? xv[i].y : e == 2 ? xv[i].z : xv[i].w;
+              acc[i][j] = __ffma2_rn(make_float2(xe, xe), ff, acc[i][j]);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();  // stage st fully read
+    if (tid == 0) issue(z + NS);
+    if (k == g.nk - 1 && active) {
+      // one division per tile; slice i+1 is 32 slices on (s += 32, carrying into m); a 64-bit row pointer and
+      // 32-bit offsets s + q*S (< Wout < 2^31)
+      const int r0 = (int)(tile * SL) + sg * 32 * RS + lane;
+      int m = r0 / g.S, sidx = r0 - m * g.S;
+      const bool fullq = q0 + QT <= g.Q;
+#pragma unroll
+      for (int i = 0; i < RS; ++i) {
+        if (i > 0) {
+          sidx += 32;
+          while (sidx >= g.S) {
+            sidx -= g.S;
+            ++m;
+          }
+        }
+        if (r0 + 32 * i < g.rows) {
+          float *yrow = Y + (int64_t)m * g.Wout;
+          asm volatile("" : "+l"(yrow));  // keep the row pointer: each store is then one IMAD.WIDE.U32 off, 4, yrow
+          uint32_t off = (uint32_t)(sidx + q0 * g.S);
+          const uint32_t S = (uint32_t)g.S;
+          if (fullq) {
+#pragma unroll
+            for (int j = 0; j < QP; ++j) {
+              st_global_f32(yrow + off, acc[i][j].x);
+              off += S;
+              st_global_f32(yrow + off, acc[i][j].y);
+              off += S;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < QP; ++j) {
+              if (q0 + 2 * j < g.Q) st_global_f32(yrow + off, acc[i][j].x);
+              off += S;
+              if (q0 + 2 * j + 1 < g.Q) st_global_f32(yrow + off, acc[i][j].y);
+              off += S;
+            }
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < QP; ++j) acc[i][j] = make_float2(0.f, 0.f);
+      }
+    }
+  }
+}
+
+template <int QT, int QR, int SG, int RS, int NS>
+int launch_sgemm_t(const PassPlan &pp, int64_t M, const void *in, void *out, const void *F, void *stream) {
+  constexpr int SL = SG * 32 * RS, QTILE = QT * QR, NT = QR * SG * 32;
+  SgemmArgs g{};
+  g.S = (int)(pp.W_in / pp.P);
+  g.rows = (int)(M * g.S);
+  g.P = pp.P;
+  g.Q = pp.Q;
+  g.Wout = (int64_t)g.S * pp.Q;
+  g.nk = (pp.P + 31) / 32;
+  g.ntiles = ((int64_t)g.rows + SL - 1) / SL;
+  CUtensorMap ta;
+  uint64_t dims[2] = {(uint64_t)pp.P, (uint64_t)g.rows};
+  uint64_t strides[1] = {(uint64_t)pp.P * 4};
+  uint32_t box[2] = {32, 256};
+  if (!encode_tmap(&ta, KRON_F32, 2, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
+  const size_t smem = 1024 + (size_t)NS * SL * 128 + (size_t)g.nk * 32 * QTILE * 4 + 8 * NS;
+  auto k = kron_sgemm_kernel<QT, QR, SG, RS, NS>;
+  const int slots = kernel_slots((const void *)k, NT, smem);
+  if (slots < 1) return (int)cudaErrorInvalidConfiguration;
+  int64_t grid = slots;
+  if (grid > g.ntiles) grid = g.ntiles;
+  k<<<(unsigned)grid, NT, smem, (cudaStream_t)stream>>>(ta, (const float *)F, (float *)out, g);
+  return (int)cudaGetLastError();
+}
+
+// QT x QR column tile and stage count of the sgemm instance for (P, Q); 0 = not eligible (the old kernel runs)
+int sgemm_pick(int64_t M, int64_t W, int P, int Q) {
+  if (P % 4 || Q % 16 || Q > 128) return 0;
+  if (M * (W / P) >= ((int64_t)1 << 31) - 1024) return 0;
+  const int nk = (P + 31) / 32;
+  if (Q <= 32) return nk * 32 * 32 * 4 <= 32768 ? 1 : 0;   // QT 8 x QR 4, 512 slices, 3 stages
+  if (Q <= 64) return nk * 32 * 64 * 4 <= 32768 ? 2 : 0;   // QT 16 x QR 4, 512 slices, 3 stages
+  return nk * 32 * 128 * 4 <= 65536 ? 3 : 0;               // QT 16 x QR 8, 256 slices, 4 stages
+}
+
 struct GemmInst {
   int dtype, BM, BN, TM, TN, NS;
 };
@@ -461,6 +653,8 @@ int launch_dmma(const PassPlan &pp, int64_t M, const void *in, void *out, const 
 }
 }  // namespace
 
+bool sgemm_supported(int64_t M, int64_t W, int P, int Q) { return sgemm_pick(M, W, P, Q) != 0; }
+
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q) {
   const int es = dtype == KRON_F32 ? 4 : 8;
   if (P < 48 || Q < 16) return false;                 // small factors: fused / generic kernels
@@ -471,6 +665,15 @@ bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q) {
 }
 
 int launch_gemm(const PassPlan &pp, int dtype, int64_t M, const void *in, void *out, const void *F, void *stream) {
+  if (dtype == KRON_F32 && pp.variant == 2) {
+    // measured on the Fig 11 workloads (tools/gpu_sgemm_var.sh): 2 CTAs of 4 warps per SM, 16 warps with RS = 4 or
+    // QT = 8, unroll 1 / 4 of the p-quad loop were all 1-10% slower than these
+    switch (sgemm_pick(M, pp.W_in, pp.P, pp.Q)) {
+      case 1: return launch_sgemm_t<8, 4, 2, 8, 3>(pp, M, in, out, F, stream);
+      case 2: return launch_sgemm_t<16, 4, 2, 8, 3>(pp, M, in, out, F, stream);
+      case 3: return launch_sgemm_t<16, 8, 1, 8, 4>(pp, M, in, out, F, stream);
+    }  // not eligible at this M: the register-tiled kernel below
+  }
   if (dtype == KRON_F64 && pp.variant == 1 && pp.P % 16 == 0 && pp.Q % 16 == 0 && !getenv("KRON_NO_DMMA"))
     return launch_dmma(pp, M, in, out, F, stream);
   const int es = dtype == KRON_F32 ? 4 : 8;

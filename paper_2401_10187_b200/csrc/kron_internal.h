@@ -48,7 +48,7 @@ struct Plan {
 // Knobs the autotuner searches over; the default policy is the static planner.
 struct PlanPolicy {
   int kcap = kMaxFused;       // largest fused group
-  unsigned kinds = 0x7FFFu;    // allowed fused kernel families (bit = FusedInstance::warp; bit 14 = chain.cu)
+  unsigned kinds = 0xFFFFu;    // allowed kernel families (bit = FusedInstance::warp; bit 14 = chain.cu; bit 15 = fp32 sgemm)
   int chain_rdiv = 1;         // chain passes: tile of R / chain_rdiv chunks (autotuner tile-size candidates)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
@@ -119,6 +119,7 @@ int launch_chain(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 bool tc_geometry(int P, int mode, int64_t W, PassPlan *pp);
 int launch_tc(const PassPlan &pp, int64_t M, const void *in, void *out, const void *const *Fgroup, void *stream);
 bool gemm_supported(int dtype, int64_t M, int64_t W, int P, int Q);
+bool sgemm_supported(int64_t M, int64_t W, int P, int Q);  // fp32 large-P pass on kron_sgemm_kernel
 
 // resident CTA slots (SMs x CTAs per SM) for a kernel launch shape; sets the dynamic-smem attribute.
 // Cached per (kernel, block, smem, device).  fused.cu

@@ -67,6 +67,12 @@ SMALL = [
     (2, [128, 16], [128, 16]),            # large P then small
     (4, [7], [9]),                        # N = 1: plain GEMM
     (3, [1, 4, 1], [2, 4, 1]),            # P_i or Q_i = 1
+    # fp32 large-P passes on kron_sgemm_kernel (the three column-tile instances, ragged tiles, idle warps)
+    (5, [64] * 3, [64] * 3),              # Fig 11 W64 shape (QT 16 x QR 4)
+    (3, [128, 128], [128, 128]),          # W128 shape (QT 16 x QR 8), 384 slices = 1.5 tiles
+    (7, [48, 64], [48, 16]),              # P = 48 (zero-padded 32-p chunk), Q = 48 / 16 (idle column ranges)
+    (2, [96, 64], [80, 32]),              # Q = 80 in a 128-column tile, Q = 32 (QT 8 x QR 4)
+    (5, [64, 3], [64, 3]),                # S = 3 slices per row: a warp's 32 slices span 11 rows
 ]
 
 
