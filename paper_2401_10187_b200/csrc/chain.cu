@@ -58,6 +58,8 @@ struct ChainArgs {
   int vec;                   // 1: 16-byte asynchronous copies (aligned rows and chunks)
   FastDiv dCP, dR;           // division by C/P (slices per chunk) and by R
   FastDiv dst[kMaxFused];    // division by P^j (step j's digit stride)
+  FastDiv dCP2;              // slice-pair path (even P, 16-byte layout): division by C/(2P)
+  FastDiv dsth[kMaxFused];   // ... and by P^j / 2
   int R;                     // chunks per tile
   int64_t W, WC;             // row width (in = out for square factors), W / C
   int64_t M, tiles_k, ntiles;
@@ -116,6 +118,55 @@ __global__ void __launch_bounds__(kChainThreads) kron_chain_kernel(const T *__re
       // slices of this step: (chunk t, hi, lo) with element base t*CS + hi*st*P + lo, elements at + p*st; a
       // thread writes its outputs over exactly the positions it read (P = Q), so a step needs no barrier
       // between its reads and writes, only one before the next step
+      if constexpr (kFReg && sizeof(T) == 4 && P % 2 == 0) {
+        if (a.vec) {
+          // even P on the 16-byte layout (CS, P, st even: every slice pair below is 8-byte aligned).
+          // Step 0 (st = 1): a slice is P contiguous values -> P/2 LDS.64 in, P/2 STS.64 out (lanes 2P words
+          // apart: the 16 lanes of a phase cover 32 distinct banks).  Steps j >= 1: a thread takes the slice
+          // PAIR (lo, lo + 1) — its elements p are adjacent — as one float2 per p and runs
+          // FFMA2(x pair, F[p][q] broadcast): half the loads, stores and index math per FMA of the scalar path
+          // (Table 4 #19, 6^7: 40% of the wavefronts were conflicts, FMA pipe at 29-40%)
+          if (j == 0) {
+            for (uint32_t sl = tid; sl < nsl; sl += kChainThreads) {
+              const uint32_t t = a.dCP.div(sl), w = sl - t * CP;
+              T *bp = buf + t * CS + w * P;
+              float x[P];
+#pragma unroll
+              for (int p = 0; p < P; p += 2) {
+                const float2 v = *reinterpret_cast<const float2 *>(bp + p);
+                x[p] = v.x;
+                x[p + 1] = v.y;
+              }
+#pragma unroll
+              for (int q = 0; q < P; q += 2) {
+                float2 acc = make_float2(x[0] * Fr[q], x[0] * Fr[q + 1]);
+#pragma unroll
+                for (int p = 1; p < P; ++p)
+                  acc = __ffma2_rn(make_float2(x[p], x[p]), make_float2(Fr[p * P + q], Fr[p * P + q + 1]), acc);
+                *reinterpret_cast<float2 *>(bp + q) = acc;
+              }
+            }
+          } else {
+            const uint32_t half = st / 2, CP2 = CP / 2;
+            for (uint32_t pr = tid; pr < nsl / 2; pr += kChainThreads) {
+              const uint32_t t = a.dCP2.div(pr), w = pr - t * CP2, hi = a.dsth[j].div(w), lo = 2 * (w - hi * half);
+              T *bp = buf + t * CS + hi * st * P + lo;
+              float2 x2[P];
+#pragma unroll
+              for (int p = 0; p < P; ++p) x2[p] = *reinterpret_cast<const float2 *>(bp + p * st);
+#pragma unroll
+              for (int q = 0; q < P; ++q) {
+                float2 acc = make_float2(x2[0].x * Fr[q], x2[0].y * Fr[q]);
+#pragma unroll
+                for (int p = 1; p < P; ++p) acc = __ffma2_rn(x2[p], make_float2(Fr[p * P + q], Fr[p * P + q]), acc);
+                *reinterpret_cast<float2 *>(bp + q * st) = acc;
+              }
+            }
+          }
+          __syncthreads();
+          continue;
+        }
+      }
       for (uint32_t sl = tid; sl < nsl; sl += kChainThreads) {
         const uint32_t t = a.dCP.div(sl), w = sl - t * CP, hi = a.dst[j].div(w), lo = w - hi * st;
         const uint32_t b = t * CS + hi * st * P + lo;
@@ -246,7 +297,11 @@ int launch_chain(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.tiles_k = a.WC / pp.R;
   a.dCP.set((uint32_t)(pp.C / pp.P));
   a.dR.set((uint32_t)pp.R);
-  for (int j = 0, st = 1; j < pp.nf; ++j, st *= pp.P) a.dst[j].set((uint32_t)st);
+  for (int j = 0, st = 1; j < pp.nf; ++j, st *= pp.P) {
+    a.dst[j].set((uint32_t)st);
+    a.dsth[j].set((uint32_t)(st > 1 ? st / 2 : 1));
+  }
+  a.dCP2.set((uint32_t)(pp.C / pp.P / 2 > 0 ? pp.C / pp.P / 2 : 1));
   a.ntiles = M * a.tiles_k;
   if (a.ntiles == 0) return 0;
   const size_t smem = chain_smem(pp.P, pp.nf, pp.C, pp.R, es, vec);
