@@ -249,7 +249,7 @@ kron_status_t plan_run(const Plan &plan, const void *X, const void *const *F, vo
 bool plan_push_ok(const Plan &plan, const PushArgs &push) {
   if (plan.passes.empty() || push.GK < 1 || push.GK > kMaxPush || push.B < 1 || push.rho < 1) return false;
   const PassPlan &pp = plan.passes.back();
-  if (pp.kind != KIND_FUSED) return false;
+  if (pp.kind != KIND_FUSED || pp.tm_in || pp.tm_out) return false;
   if (pp.W_out % push.B || push.B % push.rho || pp.W_out / push.B > kMaxPush) return false;
   const FusedInstance &fi = fused_instance(pp.variant);
   if (fi.warp == 10 || fi.warp == 12) return push.rho % 4 == 0 && push.B % 4 == 0 && push.wd % 4 == 0;
@@ -262,7 +262,7 @@ bool plan_push_ok(const Plan &plan, const PushArgs &push) {
 bool plan_remap_ok(const Plan &plan, const InRemap &rin) {
   if (plan.passes.empty() || rin.GK < 1 || rin.rho < 1) return false;
   const PassPlan &pp = plan.passes.front();
-  if (pp.kind != KIND_FUSED || fused_instance(pp.variant).warp == 7) return false;
+  if (pp.kind != KIND_FUSED || pp.tm_in || pp.tm_out || fused_instance(pp.variant).warp == 7) return false;
   const int64_t line = 128 / es_of(plan.dtype);
   if (rin.rho % line || pp.W_in % (rin.rho * rin.GK)) return false;
   const int64_t rl = rin.rho / line, bl = fused_box_lines(pp, plan.dtype);
@@ -480,6 +480,21 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     plan->passes[i].dst = dst;
   }
   for (int i = 0; i < np; ++i) plan->passes[i].src = i == 0 ? BUF_X : plan->passes[i - 1].dst;
+
+  // v11 tile-major hand-off (fused.cu, kron_tri_tm_kernel): a [16^3 triple, 16^2 pair] plan whose pair covers
+  // every remaining factor (C_B = W / C_A) passes its intermediate in tile order; single-GPU plans only (lead == 1:
+  // the distributed rounds' push / remap layouts assume the direct-index intermediate)
+  static const bool no_handoff = getenv("KRON_NO_HANDOFF") != nullptr;
+  if (np == 2 && lead == 1 && policy.handoff && !no_handoff) {
+    PassPlan &A = plan->passes[0], &B = plan->passes[1];
+    if (A.kind == KIND_FUSED && B.kind == KIND_FUSED && !A.tc_mode && !B.tc_mode &&
+        fused_instance(A.variant).warp == 12 && fused_instance(B.variant).warp == 11 && A.C == 4096 && B.C == 256 &&
+        A.W_out == B.W_in && A.C * B.C == A.W_out && (A.W_out / A.C) % 4 == 0 && B.R == 64 &&
+        (B.W_in / B.C) % B.R == 0) {
+      A.tm_out = 1;
+      B.tm_in = 1;
+    }
+  }
   return KRON_OK;
 }
 
@@ -760,12 +775,13 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
     for (size_t i = 0; i < a.passes.size(); ++i) {
       const PassPlan &x = a.passes[i], &y = b.passes[i];
       if (x.kind != y.kind || x.variant != y.variant || x.first != y.first || x.nf != y.nf || x.tileK != y.tileK ||
-          x.R != y.R ||
+          x.R != y.R || x.tm_out != y.tm_out || x.tm_in != y.tm_in ||
           x.tileM != y.tileM || x.stages != y.stages)
         return false;
     }
     return true;
   };
+  for (int ho = 1; ho >= 0; --ho)
   for (int rd : {1, 2, 4})
   for (int st = 0; st <= 1; ++st)
   for (int dm = 1; dm >= 0; --dm)
@@ -777,6 +793,7 @@ std::vector<Plan> autotune_candidates(int64_t M, int N, const int32_t *P, const 
         pol.dmma = dm == 1;
         pol.short_tiles = st == 1;
         pol.chain_rdiv = rd;
+        pol.handoff = ho == 1;
         Plan pl;
         if (make_plan(M, N, P, Q, dtype, &pl, 1, pol) != KRON_OK) continue;
         bool dup = false;
@@ -898,6 +915,8 @@ kron_status_t kron_plan_kernel(int64_t M, int32_t N, const int32_t *P, const int
                                   "kron_tc_pair_kernel"};
     const int w = fused_instance(pp.variant).warp;
     k = (w >= 0 && w < 14) ? names[w] : "kron_fused_kernel";
+    if (pp.tm_out) k = "kron_tri_tm_kernel";
+    if (pp.tm_in) k = "kron_pair_tm_kernel";
   }
   snprintf(name, (size_t)len, "%s", k);
   return KRON_OK;

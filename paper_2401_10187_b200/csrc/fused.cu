@@ -1828,6 +1828,290 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
   cluster_sync_all();  // neither CTA leaves while its peer may still read its shared memory
 }
 
+// ------------------------------------------------------------------ v11: tile-major hand-off between two fused passes
+//
+// A two-pass plan [group A, group B] whose second pass covers every remaining factor has C_B = W / C_A: pass
+// B's chunk index is pass A's composite output column u and its in-chunk index is pass A's chunk index g
+// (T[row][u*(W/C_A) + g], the direct-index layout).  With 16 KB chunks (config E's 16^3 triple)
+// the direct-index store writes 32-byte runs at a 1 KB stride — measured 3.0-3.5 TB/s, which made v10's
+// triple store-bound (10.6 ms for 34 GB).  v11 moves the permutation into pass B's TMA map instead:
+//   pass A (kron_tri_tm_kernel) writes each 4-chunk tile as ONE contiguous 64 KB block
+//       T''[row][g / 4][u][g % 4]                                   (fully coalesced 512-byte warp stores);
+//   pass B (kron_pair_tm_kernel) loads its tile of R chunks u0 .. u0+R-1 through the 3-D map
+//       {4u + g % 4, g / 4, row} with box {4R, C_B / 4, 1}          (1 KB contiguous runs per g / 4)
+// so no extra pass runs and each value still crosses HBM once out and once in.  The values are those of the
+// direct-index layout (same arithmetic, same order: results are bit-identical to the v10 plan); only the
+// intermediate's element order differs.  Y (the last pass's output) keeps the paper's layout.
+//
+// kron_tri_tm_kernel: 16 x 16 fp32 factor triples, factors in the constant bank (cb_pair16 / cb_top16 as v10),
+// one CTA per SM (no cluster, no DSMEM), tiles of 4 chunks (64 KB) through a 3-stage TMA ring; NCW compute warps
+// in groups of four (one chunk per group), four store warps.
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_tri_tm_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                        const FusedArgs a) {
+  constexpr uint32_t CE = 1024, TB = 64 * CE;  // 16 subchunks of 1 KB per chunk, 4 chunks per tile
+  constexpr int NSW = 4, C = 4096;
+  static_assert(NCW % 4 == 0, "groups of four compute warps");
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = a.stages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + (size_t)S * TB);
+  uint64_t *cdone = full + S, *empty = cdone + S;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // provably warp-uniform
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], 4 * 4 * 32);  // four chunks x four warps x 32 lanes
+      mbar_init(&empty[s], NSW * 32);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % S;
+    const int rb = (int)(tile / a.tiles_k), gq = (int)(tile - (int64_t)rb * a.tiles_k);
+    unsigned char *dst = base + (size_t)st * TB;
+    mbar_arrive_expect_tx(&full[st], TB);
+    const int line0 = gq * (4 * C / 32);
+    for (int b = 0; b < a.nbox; ++b)
+      load_in(a, dst + (size_t)b * a.box_lines * 128, &tm_in, &full[st], line0 + b * a.box_lines, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < S; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    // as v10: group grp owns one chunk at a time (chunks dealt round-robin across the tiles of the ring); warp
+    // wi runs phase 1 on subchunks 4wi .. 4wi+3, the group meets at a named barrier, then phase 2 on columns
+    // 64wi .. 64wi+63
+    constexpr int NG = NCW / 4;
+    const int grp = warp >> 2, wi = warp & 3;
+    const float *F1c = c_fac3, *F2c = c_fac3 + 256, *F3c = c_fac3 + 512;
+    for (int64_t ci = grp;; ci += NG) {
+      const int it = (int)(ci >> 2), t = (int)(ci & 3);
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      unsigned char *buf = base + (size_t)st * TB;
+      mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+      cb_pair16(buf, (uint32_t)(t * 16 + wi * 4), lane, F1c, F2c);
+      named_bar_sync(1 + grp, 128);
+      cb_top16(buf + (uint32_t)(t * 16) * CE, (uint32_t)(wi * 64 + 2 * lane), F3c);
+      __syncwarp();
+      mbar_arrive(&cdone[st]);
+    }
+  } else {
+    // store warps: lane = composite column u; OUT of chunk t at t*16 KB + (u/256)*1 KB + (swz128(4*(u%256)) ^
+    // gx(u/256)) (cb_top16's layout: 32 consecutive u = one permuted 128-byte line, conflict-free), the four
+    // chunks' values form one float4 of T''[row][gq][u][0..3]: a warp writes 512 contiguous bytes
+    const int sw = warp - NCW;
+    for (int it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      mbar_wait_sleep(&cdone[st], par);
+      const unsigned char *buf = base + (size_t)st * TB;
+      const int rb = (int)(tile / a.tiles_k), gq = (int)(tile - (int64_t)rb * a.tiles_k);
+      if (rb < a.M) {
+        float4 *yb = reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.Y) + (int64_t)rb * a.Wout + (int64_t)gq * 4 * C);
+#pragma unroll 4
+        for (int ub = sw * 32; ub < C; ub += NSW * 32) {
+          const uint32_t u = (uint32_t)(ub + lane), q3 = u >> 8;
+          const uint32_t off = q3 * CE + (swz128((u & 255u) * 4u) ^ pipe_gx<8, 4>(q3));
+          float4 v;
+          v.x = *reinterpret_cast<const float *>(buf + off);
+          v.y = *reinterpret_cast<const float *>(buf + 16 * CE + off);
+          v.z = *reinterpret_cast<const float *>(buf + 32 * CE + off);
+          v.w = *reinterpret_cast<const float *>(buf + 48 * CE + off);
+          yb[u] = v;
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&empty[st]);
+      if (sw == 0) {
+        if (lane == 0) {
+          mbar_wait_sleep(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + S);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// tm_pair16: both factors of a 16 x 16 pair on eight 256-element chunks u0 .. u0+7 of a tile loaded in the
+// tile-major order [g/4][u][g%4] (element g = 16r + c of chunk u at (4r + c/4)*1 KB + u*16 + (c%4)*4):
+//   step 1 (F1 on c): lane = chunk u0 + lane%8, rows 4(lane/8) .. +3 (two at a time, as cb_pair16): a quarter-warp
+//          reads / writes one 128-byte run of eight chunks' granules (LDS.128 / STS.128, conflict-free);
+//   step 2 (F2 on r): lane = chunk u0 + lane%8, column pair 2(2k + (lane/8)%2) .. +1 with granule k = 2kk + lane/16;
+//          16 LDS.64 over the rows, 256 FFMA2 with a factor broadcast, 16 STS.64 over the same words (OUT[q2][q1]
+//          in place of Z[s = q2][q1]); each half-warp covers one 128-byte run (conflict-free).
+// Same products and summation order as cb_pair16 (bit-identical results).
+__device__ __forceinline__ void tm_pair16(unsigned char *buf, uint32_t u0, int lane, const float *F1, const float *F2) {
+  const float4 *F1v = reinterpret_cast<const float4 *>(F1), *F2v = reinterpret_cast<const float4 *>(F2);
+  const uint32_t cu = (u0 + (uint32_t)(lane & 7)) * 16u;
+  {
+    const int rg = lane >> 3;
+#pragma unroll 1
+    for (int i = 0; i < 2; ++i) {
+      float x[2][16];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t r = (uint32_t)(rg * 4 + 2 * i + h);
+          const float4 t = *reinterpret_cast<const float4 *>(buf + (4u * r + v) * 1024u + cu);
+          x[h][4 * v] = t.x; x[h][4 * v + 1] = t.y; x[h][4 * v + 2] = t.z; x[h][4 * v + 3] = t.w;
+        }
+      float2 acc[2][8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[h][j] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < 16; ++p)
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const float4 f = F1v[p * 4 + j4];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float2 xx = make_float2(x[h][p], x[h][p]);
+            acc[h][2 * j4] = __ffma2_rn(xx, make_float2(f.x, f.y), acc[h][2 * j4]);
+            acc[h][2 * j4 + 1] = __ffma2_rn(xx, make_float2(f.z, f.w), acc[h][2 * j4 + 1]);
+          }
+        }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t r = (uint32_t)(rg * 4 + 2 * i + h);
+          *reinterpret_cast<float4 *>(buf + (4u * r + v) * 1024u + cu) =
+              make_float4(acc[h][2 * v].x, acc[h][2 * v].y, acc[h][2 * v + 1].x, acc[h][2 * v + 1].y);
+        }
+    }
+  }
+  __syncwarp();  // step 2 reads other lanes' step-1 rows
+  {
+    const uint32_t s8 = (uint32_t)((lane >> 3) & 1) * 8u;
+#pragma unroll 1
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint32_t k = (uint32_t)(2 * kk + (lane >> 4));
+      unsigned char *cb = buf + k * 1024u + cu + s8;
+      float2 x2[16];
+#pragma unroll
+      for (int r = 0; r < 16; ++r) x2[r] = *reinterpret_cast<const float2 *>(cb + (uint32_t)r * 4096u);
+      float2 acc[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const float4 f = F2v[r * 4 + q4];
+          acc[4 * q4] = __ffma2_rn(x2[r], make_float2(f.x, f.x), acc[4 * q4]);
+          acc[4 * q4 + 1] = __ffma2_rn(x2[r], make_float2(f.y, f.y), acc[4 * q4 + 1]);
+          acc[4 * q4 + 2] = __ffma2_rn(x2[r], make_float2(f.z, f.z), acc[4 * q4 + 2]);
+          acc[4 * q4 + 3] = __ffma2_rn(x2[r], make_float2(f.w, f.w), acc[4 * q4 + 3]);
+        }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) *reinterpret_cast<float2 *>(cb + (uint32_t)q * 4096u) = acc[q];
+    }
+  }
+}
+
+// kron_pair_tm_kernel: the 16 x 16 fp32 pair of pass B, input tile-major (see above), factors in the constant bank;
+// tiles of R chunks (R * 1 KB) through a TMA ring; units of eight chunks dealt round-robin to NCW compute warps
+// across tile boundaries; four store warps stream the tile out chunk-fastest to Y[row][u2*(W/C) + cb*R + u]
+// (lane = chunk: every store instruction writes one 128-byte line).
+template <int NCW>
+__global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const __grid_constant__ CUtensorMap tm_in,
+                                                                         const FusedArgs a) {
+  constexpr int NSW = 4, UC = 8;
+  const int R = a.R, UPT = R / UC;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  const int S = a.stages;
+  uint64_t *full = reinterpret_cast<uint64_t *>(base + (size_t)S * a.stage_bytes);
+  uint64_t *cdone = full + S, *empty = cdone + S;
+  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;  // provably warp-uniform
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&cdone[s], UPT * 32);
+      mbar_init(&empty[s], NSW * 32);
+    }
+    fence_mbar_init();
+    prefetch_tmap(&tm_in);
+  }
+  __syncthreads();
+  auto issue_load = [&](int it) {
+    const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+    if (tile >= a.ntiles) return;
+    const int st = it % S;
+    const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
+    mbar_arrive_expect_tx(&full[st], a.tile_bytes);
+    tma_load_3d(base + (size_t)st * a.stage_bytes, &tm_in, &full[st], cb * R * 4, 0, rb);
+  };
+  if (tid == 0)
+    for (int it = 0; it < S; ++it) issue_load(it);
+
+  if (warp < NCW) {
+    const float *F1c = c_fac2, *F2c = c_fac2 + 256;
+    for (int un = warp;; un += NCW) {
+      const int it = un / UPT, cg = un - (un / UPT) * UPT;
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      mbar_wait(&full[st], (uint32_t)((it / S) & 1));
+      tm_pair16(base + (size_t)st * a.stage_bytes, (uint32_t)(cg * UC), lane, F1c, F2c);
+      __syncwarp();
+      mbar_arrive(&cdone[st]);
+    }
+  } else {
+    const int sw = warp - NCW;
+    float *Y = reinterpret_cast<float *>(a.Y);
+    for (int it = 0;; ++it) {
+      const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
+      if (tile >= a.ntiles) break;
+      const int st = it % S;
+      const uint32_t par = (uint32_t)((it / S) & 1);
+      mbar_wait_sleep(&cdone[st], par);
+      const unsigned char *buf = base + (size_t)st * a.stage_bytes;
+      const int rb = (int)(tile / a.tiles_k), cbk = (int)(tile - (int64_t)rb * a.tiles_k);
+      if (rb < a.M) {
+        const int64_t wc = a.WC;
+        float *yr = Y + (int64_t)rb * a.Wout + (int64_t)cbk * R + lane;
+        // granule gk = 4*q2 + q1/4 holds composite columns u2 = 4*gk .. 4*gk+3 of every chunk
+#pragma unroll 1
+        for (int gk = sw; gk < 64; gk += NSW) {
+          float *p = yr + (int64_t)(4 * gk) * wc;
+          for (int h = 0; h < R / 32; ++h) {
+            const float4 v = *reinterpret_cast<const float4 *>(buf + (uint32_t)gk * 1024u + (uint32_t)(h * 32 + lane) * 16u);
+            p[h * 32] = v.x;
+            p[h * 32 + wc] = v.y;
+            p[h * 32 + 2 * wc] = v.z;
+            p[h * 32 + 3 * wc] = v.w;
+          }
+        }
+      }
+      __syncwarp();
+      mbar_arrive(&empty[st]);
+      if (sw == 0) {
+        if (lane == 0) {
+          mbar_wait_sleep(&empty[st], par);
+          fence_proxy_async_smem();
+          issue_load(it + S);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ fp64 two-factor chunks on DMMA (v5)
 //
 // The v4 sandwich OUT = F2^T . (X . F1) per 32 x 32 chunk, fp64, on the FP64 tensor cores (mma.sync
@@ -2679,6 +2963,62 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   a.stages = pp.stages;
 
   if (rin && rin->on && inst.warp == 7) return (int)cudaErrorInvalidValue;
+  if (pp.tm_out || pp.tm_in) {
+    // v11 tile-major hand-off (E-shaped [16^3 triple, 16^2 pair] plans, see kron_tri_tm_kernel)
+    if ((push && push->on) || (rin && rin->on) || dtype != KRON_F32 || pp.P != 16) return (int)cudaErrorInvalidValue;
+    CUtensorMap tin;
+    a.Y = out;
+    a.WC = WC;
+    a.Wout = Wout;
+    a.M = M;
+    Kernel4Fn kt;
+    size_t smem;
+    int threads;
+    if (pp.tm_out) {
+      if (pp.nf != 3 || WC % 4) return (int)cudaErrorInvalidValue;
+      a.tiles_k = (int)(WC / 4);
+      a.ntiles = M * a.tiles_k;
+      a.box_lines = 256;
+      a.nbox = 2;  // 4 chunks = 512 lines of 128 bytes
+      uint64_t dims[3] = {(uint64_t)line, (uint64_t)(W / line), (uint64_t)M};
+      uint64_t strides[2] = {128, (uint64_t)W * es};
+      uint32_t box[3] = {(uint32_t)line, 256u, 1u};
+      if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
+      smem = 1024 + (size_t)a.stages * 65536 + 24 * (size_t)a.stages;
+      threads = 32 * (12 + 4);
+      kt = kron_tri_tm_kernel<12>;
+    } else {
+      // T''[row][g/4][u][g%4], u < WC (this pass's chunks), g < C = 256 (the producer's chunks): box {4, R, 64, 1}
+      if (pp.nf != 2 || pp.C != 256 || pp.R != 64 || WC % pp.R) return (int)cudaErrorInvalidValue;
+      a.tiles_k = (int)(WC / pp.R);
+      a.ntiles = M * a.tiles_k;
+      a.tile_bytes = (uint32_t)pp.R * 1024u;
+      a.stage_bytes = a.tile_bytes;
+      // (u, g%4) merged into one contiguous dimension: a box row is 4R floats = 1 KB (a 16-byte inner box dimension
+      // measured 7.9 ms on E's pair pass vs 6.9 ms for the direct-index kernel)
+      uint64_t dims[3] = {(uint64_t)WC * 4, 64, (uint64_t)M};
+      uint64_t strides[2] = {(uint64_t)WC * 16, (uint64_t)W * es};
+      uint32_t box[3] = {(uint32_t)pp.R * 4, 64, 1};
+      if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
+      smem = 1024 + (size_t)a.stages * a.stage_bytes + 24 * (size_t)a.stages;
+      threads = 32 * (12 + 4);
+      kt = kron_pair_tm_kernel<12>;
+    }
+    const int kind = pp.tm_out ? 1 : 0;
+    bool capturing = false;
+    const int err = cslot_acquire((cudaStream_t)stream, kind, Fgroup, pp.nf, 256, &capturing);
+    if (err != 0) return err;
+    const int slots = kernel_slots((const void *)kt, threads, smem);
+    int lerr = (int)cudaErrorInvalidConfiguration;
+    if (slots >= 1) {
+      int64_t grid = slots;
+      if (grid > a.ntiles) grid = a.ntiles;
+      kt<<<(unsigned)grid, threads, smem, (cudaStream_t)stream>>>(tin, a);
+      lerr = (int)cudaGetLastError();
+    }
+    cslot_release((cudaStream_t)stream, kind, capturing);
+    return lerr;
+  }
   if (inst.warp == 7) {
     // 5-D map over X[m][g][s][p/16][p%16]; box = one p-half of one chunk ([64][2][16] = 16 KB)
     CUtensorMap t5;

@@ -32,6 +32,9 @@ struct PassPlan {
   int nout = 0;  // output staging buffers (warp-chain fused kernel)
   int src = BUF_X, dst = BUF_Y;
   int tc_mode = 0;  // fused pair on the tcgen05 tensor cores (tc.cu): 1 TF32, 2 3xTF32; 0 otherwise
+  // v11 tile-major hand-off (fused.cu, kron_tri_tm_kernel): this pass writes its output as T''[row][g/4][u][g%4]
+  // (tm_out) / reads its input through the matching 4-D map (tm_in) instead of the direct-index layout
+  int tm_out = 0, tm_in = 0;
 };
 
 struct Plan {
@@ -52,9 +55,10 @@ struct PlanPolicy {
   int chain_rdiv = 1;         // chain passes: tile of R / chain_rdiv chunks (autotuner tile-size candidates)
   bool dmma = true;           // fp64 large-P passes on DMMA (else register-tiled DFMA)
   bool short_tiles = false;   // v6 fp32 P = 16: 32-chunk tiles (128-byte runs, deeper ring) instead of 64-chunk
+  bool handoff = true;        // v11 tile-major hand-off between the passes of [16^3 triple, 16^2 pair] plans
   bool operator==(const PlanPolicy &o) const {
     return kcap == o.kcap && kinds == o.kinds && dmma == o.dmma && short_tiles == o.short_tiles &&
-           chain_rdiv == o.chain_rdiv;
+           chain_rdiv == o.chain_rdiv && handoff == o.handoff;
   }
 };
 kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, int dtype, Plan *out,
