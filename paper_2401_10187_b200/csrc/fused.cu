@@ -2985,8 +2985,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
       uint32_t box[3] = {(uint32_t)line, 256u, 1u};
       if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
       smem = 1024 + (size_t)a.stages * 65536 + 24 * (size_t)a.stages;
-      threads = 32 * (12 + 4);
-      kt = kron_tri_tm_kernel<12>;
+      // 16 compute warps (4 per SM sub-partition): E's triple 8.34 -> 8.13 ms vs 12 (8: 8.92)
+      static const int ncw = getenv("KRON_TRI_NCW") ? atoi(getenv("KRON_TRI_NCW")) : 16;  // A/B experiments only
+      threads = 32 * ((ncw == 16 ? 16 : ncw == 8 ? 8 : 12) + 4);
+      kt = ncw == 16 ? kron_tri_tm_kernel<16> : ncw == 8 ? kron_tri_tm_kernel<8> : kron_tri_tm_kernel<12>;
     } else {
       // T''[row][g/4][u][g%4], u < WC (this pass's chunks), g < C = 256 (the producer's chunks): box {4, R, 64, 1}
       if (pp.nf != 2 || pp.C != 256 || pp.R != 64 || WC % pp.R) return (int)cudaErrorInvalidValue;

@@ -166,6 +166,19 @@ def test_plan_kernels(kron):
     assert lib.kron_plan_kernel(16, 2, Pa, Pa, 0, 5, buf, 8) == 1   # no such pass
 
 
+def test_handoff_plans(kron):
+    # v11: a [16^3 triple, 16^2 pair] plan passes its intermediate tile-major (fused.cu kron_tri_tm_kernel); other
+    # plans, the tensor-core modes and three-factor plans keep the direct-index layout
+    assert kron.plan_kernels(4096, [16] * 5, [16] * 5, "float32") == ["kron_tri_tm_kernel", "kron_pair_tm_kernel"]
+    assert kron.plan_kernels(5, [16] * 5, [16] * 5, "float32") == ["kron_tri_tm_kernel", "kron_pair_tm_kernel"]
+    assert kron.plan_kernels(64, [16] * 6, [16] * 6, "float32") == ["kron_fused_gemm3c_kernel"] * 2
+    assert "kron_tri_tm_kernel" not in kron.plan_kernels(64, [16] * 3, [16] * 3, "float32")
+    assert kron.plan_kernels(64, [8, 16, 16, 16, 16, 16], [8, 16, 16, 16, 16, 16], "float32")[0] != "kron_tri_tm_kernel"
+    # same workspace as the direct-index plan; the autotuner also times the plan without the hand-off
+    assert kron.workspace_size(64, [16] * 5, [16] * 5, "float32") == 64 * 16 ** 5 * 4
+    assert kron.autotune_candidates(64, [16] * 5, [16] * 5, "float32") >= 2
+
+
 def test_tensor_core_mode_plans(kron):
     # the tensor-core modes (dtype codes 2 = 3xTF32, 3 = TF32) route the P = 16 / 32 fp32 square pairs to the
     # tcgen05 kernel (tc.cu); other passes stay on the fp32 CUDA-core kernels; fp64 data rejects the modes

@@ -53,7 +53,9 @@ SMALL = [
     (33, [8] * 4, [8] * 4),               # fused P=8 (3,1)
     (5, [8] * 6, [8] * 6),                # config B shape, small M (two separate passes)
     (3, [16] * 4, [16] * 4),              # fused P=16 (2,2)
-    (3, [16] * 5, [16] * 5),              # config E shape: fp32 16x16 triple on a CTA pair (v9) + pair
+    (3, [16] * 5, [16] * 5),              # config E shape: v11 triple -> pair with the tile-major hand-off
+    (1, [16] * 5, [16] * 5),              # v11 hand-off, one row (a single triple tile per 4 chunks)
+    (7, [16] * 5, [16] * 5),              # v11 hand-off, ragged row count over the persistent grid
     (5, [8, 16, 16, 16], [8, 16, 16, 16]),  # v9 triple (W = 8 chunks) behind a P=8 factor
     (2, [32] * 3, [32] * 3),              # fused P=32 (2,1)
     (9, [2] * 10, [2] * 10),              # fused P=2 deep groups
@@ -345,3 +347,40 @@ def test_host_path(kron, cuda_device, M, P, Q, dt, chunk):
     Y = kron.matmul_host(Xh, Fh, chunk_rows=chunk)
     torch.cuda.synchronize()
     assert np.array_equal(Y.numpy(), oracle.alg1(X, Fs).astype(dt))
+
+
+# ------------------------------------------------------------------ v11 tile-major hand-off (config E plans)
+
+_NOHO = """
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2401_10187_b200 import kron
+d = np.load(sys.argv[1])
+X = torch.from_numpy(d["X"]).cuda()
+Fs = [torch.from_numpy(d["F%d" % i]).cuda() for i in range(5)]
+assert kron.plan_kernels(X.shape[0], [16] * 5, [16] * 5, torch.float32) == ["kron_fused_gemm3c_kernel",
+                                                                          "kron_fused_gemm2ws_kernel"]
+np.save(sys.argv[2], kron.matmul(X, Fs).cpu().numpy())
+"""
+
+
+@pytest.mark.parametrize("M", [2, 37])
+def test_handoff_bit_identical_to_direct_index_plan(kron, cuda_device, tmp_path, M):
+    # the hand-off changes only the intermediate's element order (same products, same summation order), so Y
+    # equals the v10 direct-index plan's bit for bit on random data; the v10 plan runs in a child process with
+    # KRON_NO_HANDOFF=1 (read once per process)
+    import os
+    import subprocess
+    import sys
+    X, Fs = case(M, [16] * 5, [16] * 5, np.float32, "srand", 9)
+    assert kron.plan_kernels(M, [16] * 5, [16] * 5, "float32") == ["kron_tri_tm_kernel", "kron_pair_tm_kernel"]
+    Y = run(kron, X, Fs, cuda_device)
+    np.savez(tmp_path / "in.npz", X=X, **{"F%d" % i: f for i, f in enumerate(Fs)})
+    env = dict(os.environ, KRON_NO_HANDOFF="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.run([sys.executable, "-c", _NOHO, str(tmp_path / "in.npz"), str(tmp_path / "y.npy")], cwd=root,
+                   env=env, check=True, timeout=600)
+    Y10 = np.load(tmp_path / "y.npy")
+    assert np.array_equal(Y.view(np.uint32), Y10.view(np.uint32))
+    den = oracle.alg1(np.abs(X), [np.abs(f) for f in Fs])
+    assert float(np.max(np.abs(Y - oracle.alg1(X, Fs)) / den)) <= TOL[np.float32]
