@@ -74,6 +74,7 @@ struct FusedArgs {
 // to per-thread LDC); one array per kernel family, reused in stream order (see cslot_acquire).
 __constant__ float c_fac2[2 * 256];  // v10 pair (F1, F2)
 __constant__ float c_fac3[3 * 256];  // v10 triple (F1, F2, F3)
+__constant__ float c_fac32[1024];     // v12 P = 32 pair: F1 only (8 KB of factors thrash the constant cache)
 
 // One input box of a fused pass (rows x 128-byte lines from `line`): the plain 3-D map, or the 5-D
 // StoreGPUTile view of a receive buffer (Alg 2 line 685 done by the TMA engine's address generation).
@@ -1216,6 +1217,83 @@ __device__ __forceinline__ void cb_top16(unsigned char *cb, uint32_t c, const fl
     *reinterpret_cast<float2 *>(cb + (uint32_t)q * 1024u + (co ^ pipe_gx<8, 4>((uint32_t)q))) = acc[q];
 }
 
+// cb_pair32 (v12): both factors of a 32 x 32 fp32 pair on two 1024-element chunks g0, g0+1 of a 128B-swizzled
+// stage (row s of chunk g = one 128-byte line; element p at swz128(s*128 + 4p)).  A warp owns its two chunks:
+//   step 1 (F1 on p): lane = rows r, r+16 (r = lane % 16) of chunk g0 + lane / 16: 8 LDS.128 per row
+//          (a quarter-warp = 8 rows: distinct granules under the line XOR), out[q] = sum_p x[p] F1[p][q] as 512
+//          FFMA2 per row pair with x broadcast and a factor PAIR from a uniform register (LDCU.128 from c_fac32),
+//          written back over the row;
+//   step 2 (F2 on s): lane = column pair (2j, 2j+1), j = lane % 16, of chunk g0 + lane / 16: x2[s] = the pair in
+//          row s (LDS.64, a half-warp = one line), OUT[q2] = sum_s F2[s][q2] x2[s] as 1024 FFMA2 with the factor
+//          value broadcast from a shared-memory row of F2 (LDS.128 at one address for the whole warp: one wavefront
+//          per four FFMA2), written (after the warp's reads) at swz128(q2*128 + 8j) ^ gx(g): the chunk XOR makes
+//          the chunk-fastest stream-out reads conflict-free.
+// Only F1 sits in the constant bank: two 4 KB factors there run at 50 TFLOP/s in tools/microbench_cfma.cu (the
+// constant cache), one at 71 TFLOP/s.
+__device__ __forceinline__ void cb_pair32(unsigned char *buf, uint32_t g0, int lane, const float *F1,
+                                          const float *F2s) {
+  const float4 *F1v = reinterpret_cast<const float4 *>(F1);
+  const uint32_t g = g0 + (uint32_t)(lane >> 4), j = (uint32_t)(lane & 15);
+  unsigned char *ch = buf + g * 4096u;
+  {
+    float x[2][32];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const float4 t = *reinterpret_cast<const float4 *>(ch + swz128((j + 16u * h) * 128u + (uint32_t)v * 16u));
+        x[h][4 * v] = t.x; x[h][4 * v + 1] = t.y; x[h][4 * v + 2] = t.z; x[h][4 * v + 3] = t.w;
+      }
+    float2 acc[2][16];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc[h][k] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < 32; ++p)
+#pragma unroll
+      for (int j4 = 0; j4 < 8; ++j4) {
+        const float4 f = F1v[p * 8 + j4];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float2 xx = make_float2(x[h][p], x[h][p]);
+          acc[h][2 * j4] = __ffma2_rn(xx, make_float2(f.x, f.y), acc[h][2 * j4]);
+          acc[h][2 * j4 + 1] = __ffma2_rn(xx, make_float2(f.z, f.w), acc[h][2 * j4 + 1]);
+        }
+      }
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int v = 0; v < 8; ++v)
+        *reinterpret_cast<float4 *>(ch + swz128((j + 16u * h) * 128u + (uint32_t)v * 16u)) =
+            make_float4(acc[h][2 * v].x, acc[h][2 * v].y, acc[h][2 * v + 1].x, acc[h][2 * v + 1].y);
+  }
+  __syncwarp();
+  {
+    const uint32_t gx = pipe_gx<8, 4>(g);
+    float2 x2[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) x2[r] = *reinterpret_cast<const float2 *>(ch + swz128((uint32_t)r * 128u + j * 8u));
+    float2 acc[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) acc[q] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+#pragma unroll
+      for (int q4 = 0; q4 < 8; ++q4) {
+        const float4 f = *reinterpret_cast<const float4 *>(F2s + r * 32 + q4 * 4);
+        acc[4 * q4] = __ffma2_rn(x2[r], make_float2(f.x, f.x), acc[4 * q4]);
+        acc[4 * q4 + 1] = __ffma2_rn(x2[r], make_float2(f.y, f.y), acc[4 * q4 + 1]);
+        acc[4 * q4 + 2] = __ffma2_rn(x2[r], make_float2(f.z, f.z), acc[4 * q4 + 2]);
+        acc[4 * q4 + 3] = __ffma2_rn(x2[r], make_float2(f.w, f.w), acc[4 * q4 + 3]);
+      }
+    __syncwarp();  // the XOR'd write-back lands on other lanes' column pairs
+#pragma unroll
+    for (int q = 0; q < 32; ++q)
+      *reinterpret_cast<float2 *>(ch + (swz128((uint32_t)q * 128u + j * 8u) ^ gx)) = acc[q];
+  }
+}
+
 // ------------------------------------------------------------------ fp32 two-factor chunks, warp-specialised (v6)
 //
 // The v4 sandwich OUT = F2^T . (X . F1) per P x P chunk (P = 16 / 32, fp32), with every chunk owned by
@@ -1244,8 +1322,8 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
   constexpr int ES = 4, LINE = 32, C = P * P, PE = P * ES;
   constexpr int NSW = 4;
   constexpr int L1 = (P / RM) * (P / RN);  // lanes per chunk
-  constexpr int CPG = CB ? 4 : 32 / L1;    // chunks per warp (one work unit)
-  static_assert(!CB || P == 16, "constant-bank pairs are P = 16");
+  constexpr int CPG = CB ? (P == 16 ? 4 : 2) : 32 / L1;  // chunks per warp (one work unit)
+  static_assert(!CB || P == 16 || P == 32, "constant-bank pairs are P = 16 / 32");
   const int UPT = a.R / CPG;               // work units per tile
   constexpr uint32_t CE = C * ES;          // chunk bytes (a multiple of 1024)
   static_assert(L1 <= 32 && 32 % L1 == 0, "lane tiling");
@@ -1266,6 +1344,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
       F1s[i] = F1[i];
       *reinterpret_cast<T *>(F2Ts + swz128(c * PE + r * ES)) = F2[i];  // F2[s = r][q2 = c] -> F2T[c][r]
     }
+  } else if constexpr (P == 32) {
+    const T *F2 = reinterpret_cast<const T *>(a.F[1]);
+    for (int i = tid; i < C; i += (NCW + NSW) * 32) F1s[i] = F2[i];  // v12: F2 rows, plain (broadcast reads)
   }
   if (tid == 0) {
     for (int s = 0; s < a.stages; ++s) {
@@ -1292,15 +1373,18 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_fused_gemm2ws_kernel(c
     for (int it = 0; it < a.stages; ++it) issue_load(it);
 
   if (CB && warp < NCW) {
-    // v10 compute: each unit = two chunks through cb_pair16 (factors in the constant bank)
-    const float *F1c = c_fac2, *F2c = c_fac2 + C;
+    // v10 compute: each unit = four chunks through cb_pair16 (factors in the constant bank); v12 (P = 32): two
+    // chunks through cb_pair32 (F1 in the constant bank, F2 broadcast from shared memory)
     for (int un = warp;; un += NCW) {
       const int it = un / UPT, cg = un % UPT;
       const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
       if (tile >= a.ntiles) break;
       const int st = it % a.stages;
       mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
-      cb_pair16(base + (size_t)st * a.stage_bytes, (uint32_t)(cg * 4), lane, F1c, F2c);
+      if constexpr (P == 16)
+        cb_pair16(base + (size_t)st * a.stage_bytes, (uint32_t)(cg * CPG), lane, c_fac2, c_fac2 + 256);
+      else
+        cb_pair32(base + (size_t)st * a.stage_bytes, (uint32_t)(cg * CPG), lane, c_fac32, F1s);
       __syncwarp();
       mbar_arrive(&cdone[st]);  // every lane publishes its own writes
     }
@@ -2725,6 +2809,9 @@ const FusedInstance kInstances[] = {
     {KRON_F32, 16, 512, 2, 11, 0}, {KRON_F32, 16, 256, 2, 12, 0},
     // tcgen05 tensor-core pairs (tc.cu, TF32 / 3xTF32 modes only): ids 39 (P = 16), 40 (P = 32)
     {KRON_F32, 16, 512, 1, 13, 0}, {KRON_F32, 32, 512, 1, 13, 0},
+    // v12 (round 2): the fp32 P = 32 pair in the v6 frame with F1 in the constant bank (cb_pair32): id 41
+    // (16-chunk tiles = 64-byte output runs, 3 x 64 KB stages)
+    {KRON_F32, 32, 512, 1, 11, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -2764,6 +2851,7 @@ KernelFn instance_kernel(int i) {
     // 4 x 8 tiles on 12 warps (8 x 8 measured 7.6 -> 8.4 ms on E's pair pass)
     case 31: case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2>;
     case 37: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, false, true>;
+    case 41: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, false, true>;
     case 32: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;
@@ -2886,12 +2974,13 @@ struct CSlot {
   cudaEvent_t ev = nullptr;
   bool used = false;
 };
-CSlot g_cslots[64][2];
+CSlot g_cslots[64][3];  // kind 0: c_fac2, 1: c_fac3, 2: c_fac32
 
 int cslot_acquire(cudaStream_t s, int kind, const void *const *F, int nf, int pp, bool *capturing) {
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || nf * pp > (kind ? 768 : 512)) return (int)cudaErrorInvalidValue;
+  if (kind == 2) nf = 1;  // v12: only F1 goes to the constant bank
+  if (dev < 0 || dev >= 64 || nf * pp > (kind == 2 ? 1024 : kind ? 768 : 512)) return (int)cudaErrorInvalidValue;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) return (int)cudaGetLastError();
   *capturing = cs != cudaStreamCaptureStatusNone;
@@ -2902,7 +2991,9 @@ int cslot_acquire(cudaStream_t s, int kind, const void *const *F, int nf, int pp
     if (S.used && !*capturing && cudaStreamWaitEvent(s, S.ev, 0) != cudaSuccess) return (int)cudaGetLastError();
   }
   for (int i = 0; i < nf; ++i) {
-    const cudaError_t e = kind ? cudaMemcpyToSymbolAsync(c_fac3, F[i], (size_t)pp * sizeof(float),
+    const cudaError_t e = kind == 2 ? cudaMemcpyToSymbolAsync(c_fac32, F[i], (size_t)pp * sizeof(float), 0,
+                                                              cudaMemcpyDeviceToDevice, s)
+                          : kind ? cudaMemcpyToSymbolAsync(c_fac3, F[i], (size_t)pp * sizeof(float),
                                                          (size_t)i * pp * sizeof(float), cudaMemcpyDeviceToDevice, s)
                                : cudaMemcpyToSymbolAsync(c_fac2, F[i], (size_t)pp * sizeof(float),
                                                          (size_t)i * pp * sizeof(float), cudaMemcpyDeviceToDevice, s);
@@ -3106,7 +3197,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     a.push = *push;
   }
   // v10: this launch's factors go to a constant-bank slot first (stream-ordered)
-  const int cslot = inst.warp == 12 ? 1 : inst.warp == 11 ? 0 : -1;
+  const int cslot = inst.warp == 12 ? 1 : inst.warp == 11 ? (pp.P == 32 ? 2 : 0) : -1;
   bool capturing = false;
   if (cslot >= 0) {
     const int err = cslot_acquire((cudaStream_t)stream, cslot, Fgroup, pp.nf, pp.P * pp.P, &capturing);
@@ -3150,7 +3241,8 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   }
   KernelFn k = instance_kernel(pp.variant);
   if (a.push.on) {  // v6 / v10 pair with the fused exchange (same tiling, push epilogue)
-    k = inst.warp == 11 ? kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true, true>
+    k = inst.warp == 11 ? (pp.P == 32 ? kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, true, true>
+                                      : kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true, true>)
         : pp.P == 32    ? kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, true>
                         : kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, true>;
   }
