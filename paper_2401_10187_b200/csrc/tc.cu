@@ -18,12 +18,16 @@
 //          chunk in the chunk-fastest stream-out layout, from which four store warps write the direct-index
 //          runs Y[row][u*(W/C) + g0 + c], u = q2*P + q1.
 // Modes (reported separately from the fp32 CUDA-core path, north_star): TF32 — one MMA per K step; 3xTF32 —
-// every operand split x = hi + lo with hi = x truncated to TF32 (exact in both parts) and three MMAs
-// hi.hi + lo.hi + hi.lo accumulated in fp32 (relative error ~2^-21 per product, within the fp32 parity bar;
-// small integers are exact, so integer data stays bit-exact).
-// Warp roles (512 threads, one CTA per SM): warp 0 TMA producer, warp 1 MMA issuer (one thread) + TMEM owner,
-// warps 4-11 transform (warp w reads TMEM lanes 32*(w%4) .., the two warps of a lane quarter split the columns),
-// warps 12-15 store; warps 2-3 idle.
+// every operand split x = hi + lo with hi = x truncated to TF32 (exact in both parts) and the products
+// hi.hi + hi.lo + lo.hi (+ lo.lo) accumulated in fp32 (relative error ~2^-21 per product, within the fp32 parity
+// bar; small integers are exact, so integer data stays bit-exact).
+// Warp roles (768 threads, one CTA per SM): warp 0 TMA producer, warp 1 MMA issuer (one thread) + TMEM owner,
+// warps 4-11 and 12-19 two transform groups taking alternate tiles (warp w reads TMEM lanes 32*(w%4) .., the two
+// warps of a lane quarter split the columns; each group owns its TMEM columns and lo buffer), so one group's
+// split / Z staging / epilogue overlaps the other group's GEMMs; warps 20-23 store; warps 2-3 idle.
+// Round 2 (second version): the hi parts are never written — kind::tf32 reads only the top 19 bits of each fp32
+// operand word, so the TMA tile itself is X_hi and Z is staged once (as Z_hi) over the consumed tile, Z_lo in the
+// group's lo buffer; 3xTF32 multiplies by [F_hi | F_lo] (N = 2P) in two MMAs per K step (A = hi, A = lo).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -55,35 +59,37 @@ __device__ __forceinline__ uint32_t out_gx(uint32_t chunk) {
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 template <int P, bool X3>
-__global__ void __launch_bounds__(512, 1) kron_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_in,
+__global__ void __launch_bounds__(768, 1) kron_tc_pair_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                               const TcArgs a) {
   constexpr int C = P * P;
   constexpr uint32_t CE = C * 4;                       // chunk bytes
   constexpr uint32_t ROWB = P * 4;                     // bytes per K-major row (one slice)
   constexpr uint32_t SBO_K = 8 * ROWB;                 // 8-row swizzle atom of the K-major operands
   constexpr uint32_t LAY_K = P == 32 ? 2u : 4u;        // UMMA layout type: 128B / 64B swizzle
-  constexpr uint32_t A2M = 128 * P * 4;                // one M-tile of the MN-major Z operand
+  constexpr uint32_t A2M = 128 * P * 4;                // one M-tile of the K-major Z^T operand
   constexpr uint32_t FB = (uint32_t)C * 4 < 1024u ? 1024u : (uint32_t)C * 4;  // factor tile slot (1 KB-aligned)
-  constexpr uint32_t ID1 = umma_idesc_tf32(128, P, 0, 0);
+  // 3xTF32: B = [F_hi | F_lo] along N (the two factor tiles are adjacent K-major row blocks), so one MMA with
+  // A = X gives hi.hi | hi.lo and one with A = X_lo gives lo.hi | lo.lo; the epilogues add the two halves
+  constexpr int NB = X3 ? 2 * P : P;                   // MMA N
+  constexpr uint32_t ID1 = umma_idesc_tf32(128, NB, 0, 0);
+  constexpr int NG = 2, NTW = 8, HP = P / 2;           // transform groups, warps per group, columns per warp
   const int R = a.R, S = a.stages;
-  const uint32_t TILE = (uint32_t)R * CE;              // stage bytes
+  const uint32_t TILE = (uint32_t)R * CE;              // stage bytes (= the Z^T operand of the tile)
   const int MT = R * P / 128;                          // M-tiles of 128 rows per tile
-  const uint32_t NCOL = (uint32_t)MT * 2 * P;          // TMEM columns: D1 and D2 per M-tile
+  const uint32_t NCOL = (uint32_t)MT * 2 * NB;         // TMEM columns per group: D1 and D2 per M-tile
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  unsigned char *xlo = base + (size_t)S * TILE;                     // X lo parts (3xTF32)
-  unsigned char *a2 = xlo + (X3 ? TILE : 0u);                       // Z operand: [MT][hi, lo]
-  unsigned char *fT = a2 + (size_t)MT * A2M * (X3 ? 2 : 1);          // F1hi, F1lo, F2hi, F2lo (transposed)
+  unsigned char *xlo = base + (size_t)S * TILE;                     // per group: X lo, then Z lo (3xTF32)
+  unsigned char *fT = xlo + (X3 ? (size_t)NG * TILE : 0);           // F1hi, F1lo, F2hi, F2lo (transposed)
   uint64_t *full = reinterpret_cast<uint64_t *>(fT + 4 * FB);
   uint64_t *empty = full + S, *cdone = empty + S;
-  uint64_t *xrdy = cdone + S, *d1full = xrdy + 1, *a2rdy = d1full + 1, *d2full = a2rdy + 1;
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d2full + 1);
+  uint64_t *xrdy = cdone + S, *d1full = xrdy + NG, *a2rdy = d1full + NG, *d2full = a2rdy + NG;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(d2full + NG);
   const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
 
   // factors, transposed to K-major B operands: FT[q][p] = F[p][q] (hi / lo split in 3xTF32)
-  constexpr int NTW = 8, HP = P / 2;  // transform warps; columns per warp of a lane quarter
-  for (int i = tid; i < C; i += 512) {
+  for (int i = tid; i < C; i += 768) {
     const int p = i / P, q = i % P;
     const uint32_t o = kswz<P>((uint32_t)q * ROWB + (uint32_t)p * 4u);
     const float f1 = a.F1[i], f2 = a.F2[i];
@@ -97,16 +103,23 @@ __global__ void __launch_bounds__(512, 1) kron_tc_pair_kernel(const __grid_const
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4 * 32);    // every store lane
-      mbar_init(&cdone[s], NTW * 32);  // every transform lane
+      mbar_init(&cdone[s], NTW * 32);  // every transform lane of the tile's group
     }
-    mbar_init(xrdy, NTW * 32);
-    mbar_init(d1full, 1);
-    mbar_init(a2rdy, NTW * 32);
-    mbar_init(d2full, 1);
+    for (int g = 0; g < NG; ++g) {
+      mbar_init(&xrdy[g], NTW * 32);
+      mbar_init(&d1full[g], 1);
+      mbar_init(&a2rdy[g], NTW * 32);
+      mbar_init(&d2full[g], 1);
+    }
     fence_mbar_init();
     prefetch_tmap(&tm_in);
   }
-  if (warp == 1) tmem_alloc(tmem_slot, NCOL <= 32 ? 32u : NCOL <= 64 ? 64u : NCOL <= 128 ? 128u : 256u);
+  const uint32_t ncol_alloc = NG * NCOL <= 32    ? 32u
+                              : NG * NCOL <= 64  ? 64u
+                              : NG * NCOL <= 128 ? 128u
+                              : NG * NCOL <= 256 ? 256u
+                                                 : 512u;
+  if (warp == 1) tmem_alloc(tmem_slot, ncol_alloc);
   fence_proxy_async_smem();  // the factor tiles (generic writes) are read by the tensor cores
   tc_fence_before();
   __syncthreads();
@@ -127,125 +140,131 @@ __global__ void __launch_bounds__(512, 1) kron_tc_pair_kernel(const __grid_const
     if (lane == 0)
       for (int it = 0; it < S; ++it) issue_load(it);
   } else if (warp == 1) {
-    // ---------------- MMA issuer: GEMM1 once the tile (and its lo parts) are staged, GEMM2 once Z is staged
+    // ---------------- MMA issuer.  Tiles alternate between the two transform groups.  GEMM1's A operand is the
+    // TMA tile itself: kind::tf32 reads only the top 19 bits of each fp32 word, i.e. the truncated hi part
+    // (3xTF32 adds the MMA on the lo parts the group wrote to xlo).  MMAs into one accumulator are issued back to
+    // back (k inner): interleaving the two M-tiles' chains measured slower (C32 TF32 3.05 -> 3.34 ms).
     if (lane == 0) {
       const uint32_t fa = smem_u32(fT);
-      for (int it = 0;; ++it) {
-        const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
-        if (tile >= a.ntiles) break;
-        const int st = it % S;
-        const uint32_t ph = (uint32_t)(it & 1);
-        const uint32_t xa = smem_u32(base + (size_t)st * TILE), xl = smem_u32(xlo);
-        mbar_wait(xrdy, ph);
-        tc_fence_after();
+      auto gemm = [&](uint32_t xa, uint32_t xl, uint32_t arow, uint32_t fofs, uint32_t d0) {
         for (int i = 0; i < MT; ++i) {
-          const uint32_t d1 = tmem + (uint32_t)(i * 2 * P);
+          const uint32_t d = d0 + (uint32_t)(i * 2 * NB);
 #pragma unroll
           for (int k = 0; k < P / 8; ++k) {
-            const uint32_t ko = (uint32_t)(i * 128) * ROWB + (uint32_t)k * 32u;
-            const uint64_t ah = umma_desc(xa + ko, 16, SBO_K, LAY_K), bh = umma_desc(fa + k * 32u, 16, SBO_K, LAY_K);
-            umma_tf32(d1, ah, bh, ID1, k > 0 ? 1u : 0u);
-            if constexpr (X3) {
-              umma_tf32(d1, umma_desc(xl + ko, 16, SBO_K, LAY_K), bh, ID1, 1u);
-              umma_tf32(d1, ah, umma_desc(fa + FB + k * 32u, 16, SBO_K, LAY_K), ID1, 1u);
-            }
+            const uint32_t ko = (uint32_t)i * arow + (uint32_t)k * 32u;
+            const uint64_t bh = umma_desc(fa + fofs + k * 32u, 16, SBO_K, LAY_K);
+            umma_tf32(d, umma_desc(xa + ko, 16, SBO_K, LAY_K), bh, ID1, k > 0 ? 1u : 0u);
+            if constexpr (X3) umma_tf32(d, umma_desc(xl + ko, 16, SBO_K, LAY_K), bh, ID1, 1u);
           }
         }
-        umma_commit(d1full);
-        mbar_wait(a2rdy, ph);
-        tc_fence_after();
-        const uint32_t za = smem_u32(a2);
-        for (int i = 0; i < MT; ++i) {
-          const uint32_t d2 = tmem + (uint32_t)(i * 2 * P + P);
-          const uint32_t zh = za + (uint32_t)i * A2M * (X3 ? 2u : 1u);
-#pragma unroll
-          for (int k = 0; k < P / 8; ++k) {
-            const uint64_t ah = umma_desc(zh + (uint32_t)k * 32u, 16, SBO_K, LAY_K);
-            const uint64_t bh = umma_desc(fa + 2 * FB + k * 32u, 16, SBO_K, LAY_K);
-            umma_tf32(d2, ah, bh, ID1, k > 0 ? 1u : 0u);
-            if constexpr (X3) {
-              umma_tf32(d2, umma_desc(zh + A2M + (uint32_t)k * 32u, 16, SBO_K, LAY_K), bh, ID1, 1u);
-              umma_tf32(d2, ah, umma_desc(fa + 3 * FB + k * 32u, 16, SBO_K, LAY_K), ID1, 1u);
-            }
-          }
+      };
+      int64_t nt = 0;  // tiles of this CTA
+      for (int64_t t = blockIdx.x; t < a.ntiles; t += gridDim.x) ++nt;
+      // GEMM1 of the next tile and GEMM2 of the oldest staged one are issued in whichever order their groups get
+      // ready (polled): a fixed order made each group's epilogue wait for the other group's split
+      int i1 = 0, i2 = 0;  // next tile for GEMM1 / GEMM2 (i2 <= i1 <= i2 + 2)
+      while (i2 < nt) {
+        if (i2 < i1 && mbar_try_wait(&a2rdy[i2 & 1], (uint32_t)((i2 >> 1) & 1))) {
+          const int g = i2 & 1, st = i2 % S;
+          tc_fence_after();
+          gemm(smem_u32(base + (size_t)st * TILE), smem_u32(xlo + (size_t)g * TILE), A2M, 2 * FB,
+               tmem + (uint32_t)g * NCOL + NB);
+          umma_commit(&d2full[g]);
+          ++i2;
+        } else if (i1 < nt && i1 < i2 + 2 && mbar_try_wait(&xrdy[i1 & 1], (uint32_t)((i1 >> 1) & 1))) {
+          const int g = i1 & 1, st = i1 % S;
+          tc_fence_after();
+          gemm(smem_u32(base + (size_t)st * TILE), smem_u32(xlo + (size_t)g * TILE), 128 * ROWB, 0,
+               tmem + (uint32_t)g * NCOL);
+          umma_commit(&d1full[g]);
+          ++i1;
         }
-        umma_commit(d2full);
       }
     }
-  } else if (warp >= 4 && warp < 4 + NTW) {
-    // ---------------- transform warps: hi / lo split of the tile, D1 -> Z operand, D2 -> stream-out layout
-    const int q = warp & 3, hc = (warp - 4) >> 2, tt = (warp - 4) * 32 + lane;
-    const uint32_t lane_base = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(hc * HP);
-    for (int it = 0;; ++it) {
+  } else if (warp >= 4 && warp < 4 + NG * NTW) {
+    // ---------------- transform groups: group g takes tiles it = g, g+2, ...: lo split of X, D1 -> Z^T operand
+    // (hi = z over the consumed tile, lo = z - hi in xlo), D2 -> stream-out layout over the tile
+    const int g = (warp - 4) / NTW, wg = (warp - 4) % NTW;
+    const int q = warp & 3, hc = wg >> 2, tt = wg * 32 + lane;
+    const uint32_t lane_base = tmem + (uint32_t)g * NCOL + ((uint32_t)(32 * q) << 16) + (uint32_t)(hc * HP);
+    unsigned char *xl = xlo + (size_t)g * TILE;
+    // this warp's HP accumulator columns of D (3xTF32: the sum of the hi-factor and lo-factor halves)
+    auto ldacc = [&](uint32_t col, float (&v)[HP]) {
+      uint32_t r[HP];
+      if constexpr (P == 32) tmem_ld16(lane_base + col, r);
+      else tmem_ld8(lane_base + col, r);
+      if constexpr (X3) {
+        uint32_t r2[HP];
+        if constexpr (P == 32) tmem_ld16(lane_base + col + P, r2);
+        else tmem_ld8(lane_base + col + P, r2);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < HP; ++j) v[j] = __uint_as_float(r[j]) + __uint_as_float(r2[j]);
+      } else {
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < HP; ++j) v[j] = __uint_as_float(r[j]);
+      }
+    };
+    for (int it = g;; it += NG) {
       const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
       if (tile >= a.ntiles) break;
       const int st = it % S;
-      const uint32_t ph = (uint32_t)(it & 1);
+      const uint32_t ph = (uint32_t)((it >> 1) & 1);
       unsigned char *xt = base + (size_t)st * TILE;
       mbar_wait(&full[st], (uint32_t)((it / S) & 1));
       if constexpr (X3) {
-        for (uint32_t g = (uint32_t)tt; g < TILE / 16u; g += NTW * 32u) {
-          const float4 x = *reinterpret_cast<const float4 *>(xt + g * 16u);
-          const float4 h = make_float4(tf32_hi(x.x), tf32_hi(x.y), tf32_hi(x.z), tf32_hi(x.w));
-          *reinterpret_cast<float4 *>(xt + g * 16u) = h;
-          *reinterpret_cast<float4 *>(xlo + g * 16u) = make_float4(x.x - h.x, x.y - h.y, x.z - h.z, x.w - h.w);
+        for (uint32_t e = (uint32_t)tt; e < TILE / 16u; e += NTW * 32u) {
+          const float4 x = *reinterpret_cast<const float4 *>(xt + e * 16u);
+          *reinterpret_cast<float4 *>(xl + e * 16u) =
+              make_float4(x.x - tf32_hi(x.x), x.y - tf32_hi(x.y), x.z - tf32_hi(x.z), x.w - tf32_hi(x.w));
         }
         fence_proxy_async_smem();
       }
-      mbar_arrive(xrdy);
+      mbar_arrive(&xrdy[g]);
       // Z rows: TMEM lane 32q + lane of M-tile i is row m = i*128 + 32q + lane = (chunk c, slice s)
-      mbar_wait(d1full, ph);
+      mbar_wait(&d1full[g], ph);
       tc_fence_after();
       for (int i = 0; i < MT; ++i) {
-        uint32_t r[HP];
-        if constexpr (P == 32) tmem_ld16(lane_base + (uint32_t)(i * 2 * P), r);
-        else tmem_ld8(lane_base + (uint32_t)(i * 2 * P), r);
-        tmem_ld_wait();
+        float v[HP];
+        ldacc((uint32_t)(i * 2 * NB), v);
         const int m = 32 * q + lane, cl = m / P, s = m % P;  // chunk within the M-tile, slice
         // K-major Z^T: element (row cl*P + q1, column s) of this M-tile's operand (this warp's half of q1)
-        unsigned char *zh = a2 + (size_t)i * A2M * (X3 ? 2 : 1);
+        unsigned char *zh = xt + (size_t)i * A2M;
 #pragma unroll
         for (int j = 0; j < HP; ++j) {
           const int q1 = hc * HP + j;
           const uint32_t o = kswz<P>((uint32_t)(cl * P + q1) * ROWB + (uint32_t)s * 4u);
-          const float z = __uint_as_float(r[j]);
-          if constexpr (X3) {
-            const float h = tf32_hi(z);
-            *reinterpret_cast<float *>(zh + o) = h;
-            *reinterpret_cast<float *>(zh + A2M + o) = z - h;
-          } else {
-            *reinterpret_cast<float *>(zh + o) = z;
-          }
+          *reinterpret_cast<float *>(zh + o) = v[j];
+          if constexpr (X3) *reinterpret_cast<float *>(xl + (size_t)i * A2M + o) = v[j] - tf32_hi(v[j]);
         }
       }
       fence_proxy_async_smem();
       tc_fence_before();
-      mbar_arrive(a2rdy);
+      mbar_arrive(&a2rdy[g]);
       // OUT rows: TMEM lane of M-tile i = (chunk c, q1), registers q2 -> composite column u = q2*P + q1 of chunk
-      // c, written over the consumed tile in the stream-out layout swz128(u*4) ^ gx(c)
-      mbar_wait(d2full, ph);
+      // c, written over the tile in the stream-out layout swz128(u*4) ^ gx(c)
+      mbar_wait(&d2full[g], ph);
       tc_fence_after();
       for (int i = 0; i < MT; ++i) {
-        uint32_t r[HP];
-        if constexpr (P == 32) tmem_ld16(lane_base + (uint32_t)(i * 2 * P + P), r);
-        else tmem_ld8(lane_base + (uint32_t)(i * 2 * P + P), r);
-        tmem_ld_wait();
+        float v[HP];
+        ldacc((uint32_t)(i * 2 * NB + NB), v);
         const int m = 32 * q + lane, c = i * (128 / P) + m / P, q1 = m % P;
         unsigned char *ch = xt + (uint32_t)c * CE;
         const uint32_t gx = out_gx((uint32_t)c);
 #pragma unroll
         for (int j = 0; j < HP; ++j) {
           const uint32_t u = (uint32_t)((hc * HP + j) * P + q1);
-          *reinterpret_cast<float *>(ch + (swz128(u * 4u) ^ gx)) = __uint_as_float(r[j]);
+          *reinterpret_cast<float *>(ch + (swz128(u * 4u) ^ gx)) = v[j];
         }
       }
       tc_fence_before();
       mbar_arrive(&cdone[st]);
     }
-  } else if (warp >= 4 + NTW) {
+  } else if (warp >= 4 + NG * NTW) {
     // ---------------- store warps: chunk-fastest stream-out, Y[row][u*(W/C) + cb*R + g]: 8 consecutive chunks
     // = one 32-byte run per composite column, four columns per instruction
-    const int sw = warp - 4 - NTW;
+    const int sw = warp - 4 - NG * NTW;
     const int gl = lane & 7, uq = lane >> 3;
     for (int it = 0;; ++it) {
       const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
@@ -291,15 +310,15 @@ __global__ void __launch_bounds__(512, 1) kron_tc_pair_kernel(const __grid_const
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, NCOL <= 32 ? 32u : NCOL <= 64 ? 64u : NCOL <= 128 ? 128u : 256u);
+    tmem_dealloc(tmem, ncol_alloc);
   }
 }
 
 template <int P, bool X3>
 size_t tc_smem(int R, int S) {
-  const size_t tile = (size_t)R * P * P * 4, mt = (size_t)R * P / 128;
+  const size_t tile = (size_t)R * P * P * 4;
   const size_t fb = (size_t)P * P * 4 < 1024 ? 1024 : (size_t)P * P * 4;
-  return 1024 + (size_t)S * tile + (X3 ? tile : 0) + mt * 128 * P * 4 * (X3 ? 2 : 1) + 4 * fb + 8 * (3 * S + 4) + 16;
+  return 1024 + (size_t)S * tile + (X3 ? 2 * tile : 0) + 4 * fb + 8 * (3 * S + 8) + 16;
 }
 
 }  // namespace
@@ -358,11 +377,11 @@ int launch_tc(const PassPlan &pp, int64_t M, const void *in, void *out, const vo
                 : (x3 ? kron_tc_pair_kernel<16, true> : kron_tc_pair_kernel<16, false>);
   const size_t smem = P == 32 ? (x3 ? tc_smem<32, true>(R, S) : tc_smem<32, false>(R, S))
                               : (x3 ? tc_smem<16, true>(R, S) : tc_smem<16, false>(R, S));
-  const int slots = kernel_slots((const void *)k, 512, smem);
+  const int slots = kernel_slots((const void *)k, 768, smem);
   if (slots < 1) return (int)cudaErrorInvalidConfiguration;
   int64_t grid = slots;
   if (grid > a.ntiles) grid = a.ntiles;
-  k<<<(unsigned)grid, 512, smem, (cudaStream_t)stream>>>(tin, a);
+  k<<<(unsigned)grid, 768, smem, (cudaStream_t)stream>>>(tin, a);
   return (int)cudaGetLastError();
 }
 
