@@ -28,6 +28,10 @@
 // Round 2 (second version): the hi parts are never written — kind::tf32 reads only the top 19 bits of each fp32
 // operand word, so the TMA tile itself is X_hi and Z is staged once (as Z_hi) over the consumed tile, Z_lo in the
 // group's lo buffer; 3xTF32 multiplies by [F_hi | F_lo] (N = 2P) in two MMAs per K step (A = hi, A = lo).
+// C32 per pass: TF32 1.67 -> 1.52 ms (0.88 of HBM); 3xTF32 3.2 -> 2.20 ms (0.61 of HBM; round 1's mma.sync
+// kernel 2.78 ms).  What remains: the transform groups wait on the MMAs ~60% of their time (ncu source view);
+// with K = 8 per kind::tf32 MMA every A byte feeds only N MACs, so the operand reads, not the MMA rate, set the
+// pace (DESIGN §5 B).
 #include <cuda.h>
 #include <cuda_runtime.h>
 
