@@ -335,7 +335,8 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const int inst_tc = (tcm && p == q && allowed(13)) ? fused_find(dtype, p, 13) : -1;
     const int inst_3 = (p == q && allowed(10)) ? fused_find(dtype, p, 10) : -1;
     const int inst_3c = (p == q && allowed(12)) ? fused_find(dtype, p, 12) : -1;  // v10 triple
-    const int inst_sc = (p == q && allowed(11)) ? fused_find(dtype, p, 11) : -1;  // v10 pair
+    int inst_sc = (p == q && allowed(11)) ? fused_find(dtype, p, 11) : -1;  // v10 pair (P = 16) / v12 pair (P = 32)
+    if (inst_sc >= 0 && dtype == KRON_F32 && p == 32 && (policy.short_tiles || getenv("KRON_V12_SHORT"))) inst_sc = 42;
     int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     if (inst_s >= 0 && policy.short_tiles && dtype == KRON_F32 && p == 16) inst_s = 35;
     const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;

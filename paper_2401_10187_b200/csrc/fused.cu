@@ -2812,6 +2812,8 @@ const FusedInstance kInstances[] = {
     // v12 (round 2): the fp32 P = 32 pair in the v6 frame with F1 in the constant bank (cb_pair32): id 41
     // (16-chunk tiles = 64-byte output runs, 3 x 64 KB stages)
     {KRON_F32, 32, 512, 1, 11, 0},
+    // v12 with 8-chunk tiles (32-byte runs, 6 x 32 KB stages): id 42 (autotuner candidate, policy.short_tiles)
+    {KRON_F32, 32, 256, 1, 11, 0},
 };
 constexpr int kNumInstances = sizeof(kInstances) / sizeof(kInstances[0]);
 
@@ -2851,7 +2853,7 @@ KernelFn instance_kernel(int i) {
     // 4 x 8 tiles on 12 warps (8 x 8 measured 7.6 -> 8.4 ms on E's pair pass)
     case 31: case 35: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2>;
     case 37: return kron_fused_gemm2ws_kernel<16, 12, 4, 8, 4, 2, false, true>;
-    case 41: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, false, true>;
+    case 41: case 42: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2, false, true>;
     case 32: return kron_fused_gemm2ws_kernel<32, 8, 8, 8, 4, 2>;
     case 5: return kron_fused_warp_kernel<float, 2, 8, 256, 2>;
     case 6: return kron_fused_warp_kernel<float, 4, 4, 256, 2>;

@@ -15,7 +15,7 @@ from paper_2401_10187_b200 import kron  # noqa: E402
 
 CASES = [
     (9, [8] * 6, [8] * 6, np.float32),          # v3 factor pipeline (3,3)
-    (2, [32] * 3, [32] * 3, np.float32),        # v6 warp-specialised chunk pair, P = 32 (+ v2)
+    (2, [32] * 3, [32] * 3, np.float32),        # P = 32 chunk pair (v12 since round 2) (+ v2)
     (3, [8, 16, 16, 16], [8, 16, 16, 16], np.float32),  # v9 16x16 triple on a CTA pair (DSMEM) + v2
     (2, [16] * 4, [16] * 4, np.float32),        # v6, P = 16 (64-chunk tiles)
     (2, [16] * 3, [16] * 3, np.float32),        # v4/v6 (2) + v2 (1)
@@ -36,6 +36,10 @@ CASES = [
     (17, [32] * 3, [32] * 3, np.float32, "tf32"),               # tcgen05 pair, TF32
     (17, [32] * 3, [32] * 3, np.float32, "3xtf32"),             # tcgen05 pair, 3xTF32
     (5, [32, 16, 16], [32, 16, 16], np.float32, "3xtf32"),      # tcgen05 pair, P = 16
+    # round 2, second half
+    (3, [16] * 5, [16] * 5, np.float32, None),                  # v11 triple -> pair (tile-major hand-off)
+    (2, [32] * 4, [32] * 4, np.float32, None),                  # v12 P = 32 pairs (F1 in the constant bank)
+    (9, [32] * 4, [32] * 4, np.float32, "3xtf32"),              # tcgen05 pair v2 (two groups, polled MMAs)
 ]
 
 
