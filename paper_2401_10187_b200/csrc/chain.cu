@@ -77,9 +77,10 @@ __global__ void __launch_bounds__(kChainThreads) kron_chain_kernel(const T *__re
   const uint32_t nsl = R * CP;  // slices per tile
   // two tile buffers: the next tile's rows stream in with cp.async (LDGSTS, many copies in flight, no register
   // round trip) while this tile is multiplied and stored
-  T *bufs[2];
-  bufs[0] = Fs + ((a.k * P * P + 3) & ~3);
-  bufs[1] = bufs[0] + (size_t)R * CS;
+  // (buffer = base + cur * tile: a runtime-indexed pointer array would demote every tile access to a generic
+  // LD / ST — ncu counted them on Table 4 #19)
+  T *const buf0 = Fs + ((a.k * P * P + 3) & ~3);
+  const uint32_t tileE = R * CS;
   auto fetch = [&](int64_t tile, T *dst) {
     if (tile < a.ntiles) {
       const int64_t row = tile / a.tiles_k, tk = tile - row * a.tiles_k;
@@ -95,13 +96,13 @@ __global__ void __launch_bounds__(kChainThreads) kron_chain_kernel(const T *__re
     }
     cp_async_commit();
   };
-  fetch(blockIdx.x, bufs[0]);
+  fetch(blockIdx.x, buf0);
   int cur = 0;
   for (int64_t tile = blockIdx.x; tile < a.ntiles; tile += gridDim.x, cur ^= 1) {
     const int64_t row = tile / a.tiles_k, tk = tile - row * a.tiles_k;
     const int64_t g0 = tk * R;                         // first chunk of the tile
-    T *buf = bufs[cur];
-    fetch(tile + gridDim.x, bufs[cur ^ 1]);            // the other buffer was released at the last barrier
+    T *buf = buf0 + cur * tileE;
+    fetch(tile + gridDim.x, buf0 + (cur ^ 1) * tileE);  // the other buffer was released at the last barrier
     cp_async_wait<1>();                                // this tile's copies (all but the newest group) landed
     __syncthreads();
     uint32_t st = 1;  // stride of the digit contracted in this step (P^j)
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(kChainThreads) kron_chain_kernel(const T *__re
               }
 #pragma unroll
               for (int q = 0; q < P; q += 2) {
-                float2 acc = make_float2(x[0] * Fr[q], x[0] * Fr[q + 1]);
+                float2 acc = __fmul2_rn(make_float2(x[0], x[0]), make_float2(Fr[q], Fr[q + 1]));
 #pragma unroll
                 for (int p = 1; p < P; ++p)
                   acc = __ffma2_rn(make_float2(x[p], x[p]), make_float2(Fr[p * P + q], Fr[p * P + q + 1]), acc);
@@ -156,7 +157,7 @@ __global__ void __launch_bounds__(kChainThreads) kron_chain_kernel(const T *__re
               for (int p = 0; p < P; ++p) x2[p] = *reinterpret_cast<const float2 *>(bp + p * st);
 #pragma unroll
               for (int q = 0; q < P; ++q) {
-                float2 acc = make_float2(x2[0].x * Fr[q], x2[0].y * Fr[q]);
+                float2 acc = __fmul2_rn(x2[0], make_float2(Fr[q], Fr[q]));
 #pragma unroll
                 for (int p = 1; p < P; ++p) acc = __ffma2_rn(x2[p], make_float2(Fr[p * P + q], Fr[p * P + q]), acc);
                 *reinterpret_cast<float2 *>(bp + q * st) = acc;
@@ -256,10 +257,17 @@ bool chain_geometry(int P, int k, int dtype, int64_t W, int rdiv, PassPlan *pp) 
   if (W % C) return false;
   const int64_t WC = W / C;
   const size_t budget = 100 * 1024;
-  int best = 0;
+  int best = 0, best8 = 0;
   const bool vec = chain_vec(C, W, es);
-  for (int R = 1; R <= 16 && R <= WC; ++R)
-    if (WC % R == 0 && chain_smem(P, k, C, R, es, vec) <= budget) best = R;
+  for (int R = 1; R <= 64 && R <= WC; ++R)
+    if (WC % R == 0 && chain_smem(P, k, C, R, es, vec) <= budget) {
+      if (R <= 16) best = R;
+      if (R % 8 == 0) best8 = R;
+    }
+  // tiles of a multiple of 8 chunks, up to 64 when the chunk is small (Table 4 #19: 6^4 pass 8 chunks, 6^3 pass 48
+  // chunks = 192-byte output runs; with the shared-space and FMUL2 fixes below: 2.39 -> 2.07 ms.  Warp-owned chunks
+  // (one __syncwarp instead of a CTA barrier per step) measured no faster: 2.10 ms)
+  if (best8 > 0) best = best8;
   if (best == 0) return false;
   if (rdiv > 1) {
     int r2 = best / rdiv;

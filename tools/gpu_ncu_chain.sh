@@ -15,3 +15,8 @@ python -c "
 import json
 for d in json.load(open('gpurun_out/r02ch6/ncu_chain.json'))['launches']:
     print({k:d.get(k) for k in ['duration','fma_pipe_pct','issue_pct','smem_pct_peak','dram_gbs','registers','occupancy_pct','smem_bank_conflicts','smem_wavefronts']}, d['stalls_per_issue'])"
+python tools/ncu_stall_table.py gpurun_out/r02ch6/ncu_chain.ncu-rep gpurun_out/r02ch6/stalls_chain.json 40 > /dev/null 2>&1
+python -c "
+import json
+s=json.load(open('gpurun_out/r02ch6/stalls_chain.json')); print(s['by_opcode'])
+for t in s['top_non_fma'][:16]: print(t['samples'], t['executed'], t['sass'][:70])"
