@@ -17,6 +17,6 @@ if [ "$BENCH" = "1" ]; then
 fi
 if [ "$NCU" = "1" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv --log-file $OUT/launches_E.csv \
-     python bench.py --steps 5 --warmup 3 --no-cpu --no-e2e --no-subconfigs > /dev/null 2>&1
-  python tools/launches_summary.py $OUT/launches_E.csv > $OUT/launches_E.json 2>&1; head -c 1500 $OUT/launches_E.json
+     python bench.py --steps 5 --warmup 3 --no-autotune --no-cpu --no-e2e --no-subconfigs > /dev/null 2>&1
+  python tools/launches_summary.py $OUT/launches_E.csv $OUT/launches_E.json 2>&1 | head -8
 fi
