@@ -2220,9 +2220,12 @@ __device__ __forceinline__ uint32_t rowswzZ(uint32_t r, uint32_t c) {
 }
 
 // Warp-specialised: NCW compute warps (one chunk each per tile; with NCW = 2 * CPT two groups take
-// alternate tiles; NCW = 8 gives every SM sub-partition two DMMA warps) never stop for the HBM stream-out, which NSW
+// alternate tiles; NCW = 16 gives every SM sub-partition four DMMA warps) never stop for the HBM stream-out, which NSW
 // store warps do from the finished tile while the compute warps work on the next ones (mbarriers:
 // full = TMA landed, cdone = chunks computed, empty = tile streamed out -> refill).
+// Round 2: GEMM1 by row halves and GEMM2 by column halves, each half's results written right away (Z rows depend
+// only on their own X rows; an OUT column half only on the Z columns of that half) — half the accumulator
+// registers (96), so two tile groups of 8 compute warps fit (NCW = 16): C64 9.00 -> 8.75 ms
 template <int NCW, int NSW, int CPT>
 __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(const __grid_constant__ CUtensorMap tm_in,
                                                                              const FusedArgs a) {
@@ -2281,72 +2284,71 @@ __global__ void __launch_bounds__((NCW + NSW) * 32, 1) kron_fused_dmma2_kernel(c
       const int st = it % a.stages;
       mbar_wait(&full[st], (uint32_t)((it / a.stages) & 1));
       unsigned char *cb0 = base + (size_t)st * a.stage_bytes + (uint32_t)g * CB;
-      double acc[2][4][4];
-      // ---- GEMM1: Z[s][q1] = sum_p X[s][p] F1[p][q1]
+      {
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+        for (int mt = 0; mt < 2; ++mt) {  // GEMM1, rows 16mt..16mt+15 (they read only their own X rows)
+          double acc1[4][4];
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+          for (int nt = 0; nt < 4; ++nt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+            for (int e = 0; e < 4; ++e) acc1[nt][e] = 0.0;
 #pragma unroll
-      for (int k0 = 0; k0 < P; k0 += 4) {
-        double a0[2], a1[2], b[4];
+          for (int k0 = 0; k0 < P; k0 += 4) {
+            const double a0 = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq, k0 + tq));
+            const double a1 = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq + 8, k0 + tq));
+            double b[4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          a0[mt] = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq, k0 + tq));
-          a1[mt] = *reinterpret_cast<const double *>(cb0 + rowswz32(mt * 16 + gq + 8, k0 + tq));
+            for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(F1s + rowswz32(k0 + tq, nt * 8 + gq));
+#pragma unroll
+            for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc1[nt], a0, a1, b[nt]);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+            for (int v1 = 0; v1 < 2; ++v1)
+              *reinterpret_cast<double2 *>(cb0 + rowswzZ(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
+                  make_double2(acc1[nt][2 * v1], acc1[nt][2 * v1 + 1]);
         }
+        __syncwarp();
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(F1s + rowswz32(k0 + tq, nt * 8 + gq));
+        for (int nq = 0; nq < 2; ++nq) {  // GEMM2, columns 16nq..16nq+15 (OUT stays inside those columns' lines)
+          double acc2[2][2][4];
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
+          for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[mt][nt], a0[mt], a1[mt], b[nt]);
-      }
-      __syncwarp();
+            for (int nt = 0; nt < 2; ++nt)
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+              for (int e = 0; e < 4; ++e) acc2[mt][nt][e] = 0.0;
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+          for (int k0 = 0; k0 < P; k0 += 4) {
+            double a0[2], a1[2], b[2];
 #pragma unroll
-          for (int v1 = 0; v1 < 2; ++v1)
-            *reinterpret_cast<double2 *>(cb0 + rowswzZ(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq)) =
-                make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
-      __syncwarp();
-      // ---- GEMM2: OUT[q2][q1] = sum_s F2T[q2][s] Z[s][q1]
+            for (int mt = 0; mt < 2; ++mt) {
+              a0[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq, k0 + tq));
+              a1[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq + 8, k0 + tq));
+            }
 #pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
+            for (int nt = 0; nt < 2; ++nt)
+              b[nt] = *reinterpret_cast<const double *>(cb0 + rowswzZ(k0 + tq, nq * 16 + nt * 8 + gq));
 #pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
+            for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[mt][nt][e] = 0.0;
+              for (int nt = 0; nt < 2; ++nt) dmma_m16n8k4(acc2[mt][nt], a0[mt], a1[mt], b[nt]);
+          }
+          __syncwarp();
 #pragma unroll
-      for (int k0 = 0; k0 < P; k0 += 4) {
-        double a0[2], a1[2], b[4];
+          for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-        for (int mt = 0; mt < 2; ++mt) {
-          a0[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq, k0 + tq));
-          a1[mt] = *reinterpret_cast<const double *>(F2Ts + rowswz32(mt * 16 + gq + 8, k0 + tq));
+            for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+              for (int v1 = 0; v1 < 2; ++v1)
+                *reinterpret_cast<double2 *>(cb0 + (rowswzZ(mt * 16 + gq + 8 * v1, nq * 16 + nt * 8 + 2 * tq) ^ gx)) =
+                    make_double2(acc2[mt][nt][2 * v1], acc2[mt][nt][2 * v1 + 1]);
         }
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt) b[nt] = *reinterpret_cast<const double *>(cb0 + rowswzZ(k0 + tq, nt * 8 + gq));
-#pragma unroll
-        for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-          for (int nt = 0; nt < 4; ++nt) dmma_m16n8k4(acc[mt][nt], a0[mt], a1[mt], b[nt]);
+        __syncwarp();
+        mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
       }
-      __syncwarp();
-#pragma unroll
-      for (int mt = 0; mt < 2; ++mt)
-#pragma unroll
-        for (int nt = 0; nt < 4; ++nt)
-#pragma unroll
-          for (int v1 = 0; v1 < 2; ++v1)
-            *reinterpret_cast<double2 *>(cb0 + (rowswzZ(mt * 16 + gq + 8 * v1, nt * 8 + 2 * tq) ^ gx)) =
-                make_double2(acc[mt][nt][2 * v1], acc[mt][nt][2 * v1 + 1]);
-      __syncwarp();
-      mbar_arrive(&cdone[st]);  // every lane: each publishes its own writes
     }
   } else {
     // ---------------- store warps: chunk-fastest stream-out, Y[row][u*(W/C) + cb*R + g]
@@ -2822,7 +2824,7 @@ using Kernel4Fn = void (*)(const CUtensorMap, const FusedArgs);
 
 Kernel4Fn instance_kernel4(int i) {
   switch (i) {
-    case 30: return kron_fused_dmma2_kernel<8, 4, 8>;
+    case 30: return kron_fused_dmma2_kernel<16, 4, 8>;
     case 33: return kron_fused_dmma2g_kernel<8, 4>;
     case 34: return kron_fused_tf32x3_kernel<8, 4>;
     case 36: return kron_fused_gemm3c_kernel<12>;
@@ -3180,7 +3182,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   if (inst.warp == 5 || inst.warp == 8) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + (inst.warp == 8 ? 4 : 2) * (size_t)pp.P * pp.P * es +
            24 * (size_t)a.stages;
-    threads = 32 * (8 + 4);
+    threads = 32 * ((inst.warp == 5 ? 16 : 8) + 4);  // v5: two tile groups of 8 compute warps
   } else if (inst.warp == 6 || inst.warp == 11) {
     smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * (size_t)pp.P * pp.P * es + 24 * (size_t)a.stages;
     threads = 32 * ((pp.P == 32 ? 8 : 12) + 4);  // compute warps of the instance (see instance_kernel)
