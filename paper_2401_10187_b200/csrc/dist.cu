@@ -140,6 +140,29 @@ __global__ void __launch_bounds__(256) dist_store_gpu_tile_kernel(const T *__res
   }
 }
 
+// The same StoreGPUTile copy by whole runs (rho >= 64): one CTA per run, 16-byte copies when the runs are
+// 16-byte aligned — the per-element kernel above spends three 64-bit divisions per value (config E's final
+// remap, rho = 2048: 5.4 ms for 8.6 GB through the virtual backend)
+template <typename T>
+__global__ void __launch_bounds__(256) dist_store_gpu_tile_runs_kernel(const T *__restrict__ recv, T *__restrict__ out,
+                                                                       int64_t rows, int64_t Wl, int64_t rho, int GK,
+                                                                       int vec) {
+  const int64_t B = Wl / GK, nrun = Wl / rho, total = rows * nrun;
+  for (int64_t r = blockIdx.x; r < total; r += gridDim.x) {
+    const int64_t m = r / nrun, run = r - m * nrun;
+    const int64_t e = run / GK, src = run - e * GK;
+    const T *sp = recv + (src * rows + m) * B + e * rho;
+    T *dp = out + m * Wl + run * rho;
+    if (vec) {
+      const int n4 = (int)(rho * (int64_t)sizeof(T) / 16);
+      for (int i = threadIdx.x; i < n4; i += blockDim.x)
+        reinterpret_cast<float4 *>(dp)[i] = reinterpret_cast<const float4 *>(sp)[i];
+    } else {
+      for (int i = threadIdx.x; i < (int)rho; i += blockDim.x) dp[i] = sp[i];
+    }
+  }
+}
+
 int launch_pack(int dtype, const void *in, void *send, int64_t rows, int64_t Wl, int64_t B, cudaStream_t s) {
   const int64_t n = rows * Wl;
   if (n == 0) return 0;
@@ -156,6 +179,22 @@ int launch_store_gpu_tile(int dtype, const void *recv, void *out, int64_t rows, 
                           cudaStream_t s) {
   const int64_t n = rows * Wl;
   if (n == 0) return 0;
+  if (rho >= 64 && Wl % rho == 0 && rho < (int64_t(1) << 30)) {
+    const size_t es = dtype == KRON_F32 ? 4 : 8;
+    const int vec = ((uintptr_t)recv % 16 == 0 && (uintptr_t)out % 16 == 0 && (rho * (int64_t)es) % 16 == 0 &&
+                     ((Wl / GK) * (int64_t)es) % 16 == 0 && (Wl * (int64_t)es) % 16 == 0)
+                        ? 1
+                        : 0;
+    int64_t blocks = rows * (Wl / rho);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (dtype == KRON_F32)
+      dist_store_gpu_tile_runs_kernel<float><<<(unsigned)blocks, 256, 0, s>>>((const float *)recv, (float *)out, rows,
+                                                                              Wl, rho, GK, vec);
+    else
+      dist_store_gpu_tile_runs_kernel<double><<<(unsigned)blocks, 256, 0, s>>>((const double *)recv, (double *)out,
+                                                                               rows, Wl, rho, GK, vec);
+    return (int)cudaGetLastError();
+  }
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (dtype == KRON_F32)
@@ -388,6 +427,7 @@ struct RoundPlan {
   int64_t wl_in = 0, wl_out = 0, rho = 0;
   bool fpush = false;   // backends 0/1: the last pass writes the destination-major send buffer
   bool fremap = false;  // backends 0/1: the first pass reads the previous round's receive buffer in place
+  int tm = 0;           // backends 0/1, config-E rounds [16^3, 16^2]: v11 tile-major layouts (1 triple, 2 pair)
 };
 
 inline char *at(void *p, int64_t elems, size_t es) { return static_cast<char *>(p) + (size_t)elems * es; }
@@ -852,6 +892,29 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
       max_w = std::max(max_w, std::max(R.wl_in, R.wl_out));
       f -= R.k;
     }
+    // v11 hand-off through the exchange (fused.cu kron_tri_tm_kernel): rounds [16^3 triple, 16^2 pair] on fp32 —
+    // the triple writes the send blocks tile-major (each destination's u range), the pair reads the receive
+    // blocks through a 4-D map whose box lands in the single-GPU tile layout, and pushes its outputs into the
+    // final send blocks; the values and the exchanged volume are those of the direct-index rounds
+    static const bool no_handoff = getenv("KRON_NO_HANDOFF") != nullptr;
+    bool tm = !p2p && ctx->fused && !no_handoff && dtype == KRON_F32 && rounds.size() == 2 && rounds[0] == 3 &&
+              rounds[1] == 2 && GK <= kMaxPush && 64 % GK == 0;
+    for (int i = 0; i < N; ++i) tm &= P[i] == 16 && Q[i] == 16;
+    for (int j = 0; j < 2 && tm; ++j)
+      for (int v = 0; v < 2; ++v) {
+        const Plan &pl = rp[j].plan[v];
+        tm &= pl.passes.size() == 1 && pl.passes[0].kind == KIND_FUSED && !pl.passes[0].tc_mode &&
+              fused_instance(pl.passes[0].variant).warp == (j == 0 ? 12 : 11) && pl.passes[0].R == (j == 0 ? 8 : 64);
+      }
+    if (tm) {
+      tm &= (rp[0].wl_in / 4096) % 4 == 0 && 4096 % (32 * GK) == 0 && (rp[1].wl_in / 256) % 64 == 0;
+    }
+    if (tm) {
+      rp[0].tm = 1;
+      rp[1].tm = 2;
+      need_out = false;
+      need_cur = false;
+    }
   }
   const size_t buf_bytes = (size_t)Ml * max_w * es;
   size_t half = 0;
@@ -931,6 +994,34 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
       if (j > 0 && nccl_be && cudaStreamWaitEvent(s, ev[2 + 2 * c], 0) != cudaSuccess) st = KRON_ERR_CUDA;
       for (int r = 0; r < nranks && st == KRON_OK; ++r) {
         RankBufs &b = bufs[r];
+        if (R.tm) {
+          // v11 rounds: one kernel each, exchange layouts written / read by the kernels themselves
+          PassPlan pp = plan.passes[0];
+          const void *grp[kMaxFused];
+          for (int k = 0; k < pp.nf; ++k) grp[k] = Fj[pp.first - 1 - k];
+          char *send = at(b.send, r0 * R.wl_out, es);
+          PushArgs pa;
+          for (int d = 0; d < GK; ++d) pa.dst[d] = send + (size_t)d * blk * es;
+          pa.B = pa.rho = R.tm == 1 ? pp.Qc / GK : B;
+          pa.wd = pa.B;
+          pa.GK = 1;
+          pa.me = 0;
+          pa.on = 1;
+          InRemap ri;
+          int err;
+          if (R.tm == 1) {
+            pp.tm_out = 1;
+            err = launch_fused(pp, (int)dtype, rows, at(Xv[r], r0 * Kl, es), send, grp, s, &pa, nullptr);
+          } else {
+            pp.tm_in = 1;
+            ri.rho = rp[j - 1].rho;
+            ri.GK = GK;
+            ri.on = 1;
+            err = launch_fused(pp, (int)dtype, rows, at(b.recv, r0 * R.wl_in, es), send, grp, s, &pa, &ri);
+          }
+          if (err != 0) st = KRON_ERR_CUDA;
+          continue;
+        }
         // this chunk's input: X, the previous round's receive block (remapped view) or its StoreGPUTile copy
         const void *in;
         InRemap ri;

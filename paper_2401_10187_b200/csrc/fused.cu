@@ -2000,6 +2000,10 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_tri_tm_kernel(const __
       const unsigned char *buf = base + (size_t)st * TB;
       const int rb = (int)(tile / a.tiles_k), gq = (int)(tile - (int64_t)rb * a.tiles_k);
       if (rb < a.M) {
+        // single GPU: one block T''[row][gq][u][4]; distributed round (push.on): the u range split over the GK
+        // destinations, send[d][row][gq][u - d*Ud][4] (Ud = push.B composite columns per destination: the
+        // round's destination-major send block in the tile-major order the next round's map reads)
+        const int64_t Ud = a.push.on ? a.push.B : C;
         float4 *yb = reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.Y) + (int64_t)rb * a.Wout + (int64_t)gq * 4 * C);
 #pragma unroll 4
         for (int ub = sw * 32; ub < C; ub += NSW * 32) {
@@ -2010,7 +2014,13 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_tri_tm_kernel(const __
           v.y = *reinterpret_cast<const float *>(buf + 16 * CE + off);
           v.z = *reinterpret_cast<const float *>(buf + 32 * CE + off);
           v.w = *reinterpret_cast<const float *>(buf + 48 * CE + off);
-          yb[u] = v;
+          if (a.push.on) {
+            const int d = ub / (int)Ud;  // warp-uniform: Ud is a multiple of 32
+            float4 *sb = reinterpret_cast<float4 *>(a.push.dst[d]) + ((int64_t)rb * a.tiles_k + gq) * Ud;
+            sb[u - (int64_t)d * Ud] = v;
+          } else {
+            yb[u] = v;
+          }
         }
       }
       __syncwarp();
@@ -2138,7 +2148,9 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
     const int st = it % S;
     const int rb = (int)(tile / a.tiles_k), cb = (int)(tile - (int64_t)rb * a.tiles_k);
     mbar_arrive_expect_tx(&full[st], a.tile_bytes);
-    tma_load_3d(base + (size_t)st * a.stage_bytes, &tm_in, &full[st], cb * R * 4, 0, rb);
+    // distributed round: the map has a 4th dimension, the source rank of the receive buffer (rmp_GK sources)
+    if (a.rmp_GK) tma_load_4d(base + (size_t)st * a.stage_bytes, &tm_in, &full[st], cb * R * 4, 0, rb, 0);
+    else tma_load_3d(base + (size_t)st * a.stage_bytes, &tm_in, &full[st], cb * R * 4, 0, rb);
   };
   if (tid == 0)
     for (int it = 0; it < S; ++it) issue_load(it);
@@ -2175,10 +2187,24 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
           float *p = yr + (int64_t)(4 * gk) * wc;
           for (int h = 0; h < R / 32; ++h) {
             const float4 v = *reinterpret_cast<const float4 *>(buf + (uint32_t)gk * 1024u + (uint32_t)(h * 32 + lane) * 16u);
-            p[h * 32] = v.x;
-            p[h * 32 + wc] = v.y;
-            p[h * 32 + 2 * wc] = v.z;
-            p[h * 32 + 3 * wc] = v.w;
+            if (a.push.on) {
+              // distributed round: column c = u2*wc + chunk goes to destination d = c / B of the send block
+              // send[d][row][B] (the pack fused into the store, as the v6 / v10 PUSH epilogues with rho = B, GK = 1);
+              // with B a multiple of wc (push.B = W / GK, wc = W / 256) d = u2 / (B / wc), no 64-bit division
+              const float vv[4] = {v.x, v.y, v.z, v.w};
+              const int upd = (int)(a.push.B / wc);  // composite columns u2 per destination
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const int u2 = 4 * gk + j, d = u2 / upd;
+                const int64_t e = (int64_t)(u2 - d * upd) * wc + (int64_t)cbk * R + h * 32 + lane;
+                reinterpret_cast<float *>(a.push.dst[d])[(int64_t)rb * a.push.B + e] = vv[j];
+              }
+            } else {
+              p[h * 32] = v.x;
+              p[h * 32 + wc] = v.y;
+              p[h * 32 + 2 * wc] = v.z;
+              p[h * 32 + 3 * wc] = v.w;
+            }
           }
         }
       }
@@ -3059,8 +3085,15 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
 
   if (rin && rin->on && inst.warp == 7) return (int)cudaErrorInvalidValue;
   if (pp.tm_out || pp.tm_in) {
-    // v11 tile-major hand-off (E-shaped [16^3 triple, 16^2 pair] plans, see kron_tri_tm_kernel)
-    if ((push && push->on) || (rin && rin->on) || dtype != KRON_F32 || pp.P != 16) return (int)cudaErrorInvalidValue;
+    // v11 tile-major hand-off (E-shaped [16^3 triple, 16^2 pair] plans, see kron_tri_tm_kernel).  Distributed
+    // rounds (kron_matmul_dist): the triple pushes into the destination-major send blocks (push->B = composite
+    // columns per destination), the pair reads the receive blocks through a 4-D map (rin->GK sources) and pushes
+    // its outputs into the next send blocks (push->B = values per row and destination)
+    if (dtype != KRON_F32 || pp.P != 16 || (rin && rin->on && !pp.tm_in)) return (int)cudaErrorInvalidValue;
+    if (push && push->on) {
+      if (push->GK != 1 || push->rho != push->B || push->B < 1) return (int)cudaErrorInvalidValue;
+      a.push = *push;
+    }
     CUtensorMap tin;
     a.Y = out;
     a.WC = WC;
@@ -3071,6 +3104,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     int threads;
     if (pp.tm_out) {
       if (pp.nf != 3 || WC % 4) return (int)cudaErrorInvalidValue;
+      if (a.push.on && (pp.Qc % a.push.B || a.push.B % 32 || pp.Qc / a.push.B > kMaxPush)) return (int)cudaErrorInvalidValue;
       a.tiles_k = (int)(WC / 4);
       a.ntiles = M * a.tiles_k;
       a.box_lines = 256;
@@ -3087,16 +3121,29 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     } else {
       // T''[row][g/4][u][g%4], u < WC (this pass's chunks), g < C = 256 (the producer's chunks): box {4, R, 64, 1}
       if (pp.nf != 2 || pp.C != 256 || pp.R != 64 || WC % pp.R) return (int)cudaErrorInvalidValue;
+      if (a.push.on && (a.push.B % WC || (pp.Qc * WC) % a.push.B)) return (int)cudaErrorInvalidValue;
       a.tiles_k = (int)(WC / pp.R);
       a.ntiles = M * a.tiles_k;
       a.tile_bytes = (uint32_t)pp.R * 1024u;
       a.stage_bytes = a.tile_bytes;
       // (u, g%4) merged into one contiguous dimension: a box row is 4R floats = 1 KB (a 16-byte inner box dimension
       // measured 7.9 ms on E's pair pass vs 6.9 ms for the direct-index kernel)
-      uint64_t dims[3] = {(uint64_t)WC * 4, 64, (uint64_t)M};
-      uint64_t strides[2] = {(uint64_t)WC * 16, (uint64_t)W * es};
-      uint32_t box[3] = {(uint32_t)pp.R * 4, 64, 1};
-      if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
+      if (rin && rin->on) {
+        // receive blocks recv[src][row][gq][u][4], gq < 64 / GK: box {4R, 64 / GK, 1, GK} lands as [g/4][u][g%4]
+        // with g/4 = src * (64 / GK) + gq — the single-GPU tile layout
+        const int64_t GK = rin->GK, Gs = 64 / GK;
+        if (GK < 1 || 64 % GK || W % GK) return (int)cudaErrorInvalidValue;
+        uint64_t dims[4] = {(uint64_t)WC * 4, (uint64_t)Gs, (uint64_t)M, (uint64_t)GK};
+        uint64_t strides[3] = {(uint64_t)WC * 16, (uint64_t)(W / GK) * es, (uint64_t)M * (uint64_t)(W / GK) * es};
+        uint32_t box[4] = {(uint32_t)pp.R * 4, (uint32_t)Gs, 1, (uint32_t)GK};
+        if (!encode_tmap(&tin, dtype, 4, in, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
+        a.rmp_GK = (int)GK;
+      } else {
+        uint64_t dims[3] = {(uint64_t)WC * 4, 64, (uint64_t)M};
+        uint64_t strides[2] = {(uint64_t)WC * 16, (uint64_t)W * es};
+        uint32_t box[3] = {(uint32_t)pp.R * 4, 64, 1};
+        if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, false)) return (int)cudaErrorInvalidValue;
+      }
       smem = 1024 + (size_t)a.stages * a.stage_bytes + 24 * (size_t)a.stages;
       threads = 32 * (12 + 4);
       kt = kron_pair_tm_kernel<12>;

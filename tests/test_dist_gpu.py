@@ -109,3 +109,20 @@ def test_dist_layout_errors(kron, cuda_device):
     ctx.close()
     with pytest.raises(kron.KronError):
         kron.DistContext("virtual", world_size=6)  # grid rule does not yield 6 GPUs (G14)
+
+
+@pytest.mark.parametrize("GM,GK,M", [(1, 2, 4), (2, 4, 8), (1, 8, 3)])
+def test_dist_config_e_tile_major_rounds(kron, cuda_device, GM, GK, M):
+    # v11 through the exchange: round 1's triple writes the send blocks tile-major, round 2's pair reads the
+    # receive blocks through a 4-D map (a source-rank dimension) and pushes into the final send blocks — the
+    # kernels must be the tile-major ones and every rank's block bit-exact on integer data
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        res = run_virtual(kron, cuda_device, GM, GK, M, [16] * 5, [16] * 5, np.float32, "int1", 2, True)
+        torch.cuda.synchronize()
+    names = " ".join(e.name for e in prof.events())
+    assert "kron_tri_tm_kernel" in names and "kron_pair_tm_kernel" in names
+    assert "gemm3c" not in names and "store_gpu_tile" in names  # only the final remap into Y_local
+    for y, ref in res:
+        assert np.array_equal(y, ref.astype(np.float32))
