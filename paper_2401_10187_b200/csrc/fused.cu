@@ -2191,14 +2191,14 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
               // distributed round: column c = u2*wc + chunk goes to destination d = c / B of the send block
               // send[d][row][B] (the pack fused into the store, as the v6 / v10 PUSH epilogues with rho = B, GK = 1);
               // with B a multiple of wc (push.B = W / GK, wc = W / 256) d = u2 / (B / wc), no 64-bit division
+              // (B / wc = 256 / GK composite columns per destination, a power of two: shifts, no division)
               const float vv[4] = {v.x, v.y, v.z, v.w};
-              const int upd = (int)(a.push.B / wc);  // composite columns u2 per destination
+              const int ush = __ffs((int)(a.push.B / wc)) - 1;
+              const int d = (4 * gk) >> ush;  // the four columns 4gk .. 4gk+3 share a destination (B / wc >= 4)
+              float *sd = reinterpret_cast<float *>(a.push.dst[d]) + (int64_t)rb * a.push.B + (int64_t)cbk * R + h * 32 +
+                          lane + (int64_t)((4 * gk) & ((1 << ush) - 1)) * wc;
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int u2 = 4 * gk + j, d = u2 / upd;
-                const int64_t e = (int64_t)(u2 - d * upd) * wc + (int64_t)cbk * R + h * 32 + lane;
-                reinterpret_cast<float *>(a.push.dst[d])[(int64_t)rb * a.push.B + e] = vv[j];
-              }
+              for (int j = 0; j < 4; ++j) sd[(int64_t)j * wc] = vv[j];
             } else {
               p[h * 32] = v.x;
               p[h * 32 + wc] = v.y;
@@ -3121,7 +3121,10 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
     } else {
       // T''[row][g/4][u][g%4], u < WC (this pass's chunks), g < C = 256 (the producer's chunks): box {4, R, 64, 1}
       if (pp.nf != 2 || pp.C != 256 || pp.R != 64 || WC % pp.R) return (int)cudaErrorInvalidValue;
-      if (a.push.on && (a.push.B % WC || (pp.Qc * WC) % a.push.B)) return (int)cudaErrorInvalidValue;
+      if (a.push.on) {
+        const int64_t upd = a.push.B / WC;  // composite columns per destination: a power of two >= 4
+        if (a.push.B % WC || (pp.Qc * WC) % a.push.B || upd < 4 || (upd & (upd - 1))) return (int)cudaErrorInvalidValue;
+      }
       a.tiles_k = (int)(WC / pp.R);
       a.ntiles = M * a.tiles_k;
       a.tile_bytes = (uint32_t)pp.R * 1024u;
