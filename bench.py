@@ -335,8 +335,26 @@ def run_sweep(args):
             gms = e0.elapsed_time(e1) / args.steps
             g.close()
             line.update({"graph_ms": round(gms, 5), "graph_gflops": round(fl / gms / 1e6, 2)})
+            # the autotuner on the same buffers: every candidate plan timed, the fastest installed
+            # in the plan cache, then the call timed again through it
+            _, ncand, _ = kron.autotune(X, Fs, out=Y, reps=3)
+            del work  # the tuned plan may need another workspace size
+            wt = torch.empty(max(kron.workspace_size(M, P, Q, tdt), 1), dtype=torch.uint8, device=dev)
+            for _ in range(args.warmup):
+                kron.matmul_ws(X, Fs, Y, wt)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(args.steps):
+                kron.matmul_ws(X, Fs, Y, wt)
+            e1.record()
+            torch.cuda.synchronize()
+            tms = e0.elapsed_time(e1) / args.steps
+            line.update({"tuned_ms": round(tms, 5), "tuned_gflops": round(fl / tms / 1e6, 2), "tuned_candidates": ncand,
+                         "tuned_plan": [list(p) for p in kron.plan_describe(M, P, Q, tdt)],
+                         "tuned_kernels": kron.plan_kernels(M, P, Q, tdt)})
+            kron.plan_cache_clear()
             print(json.dumps(line), flush=True)
-            del X, Y, work, Fs
+            del X, Y, wt, Fs
             torch.cuda.empty_cache()
     return 0
 

@@ -339,7 +339,11 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     if (inst_sc >= 0 && dtype == KRON_F32 && p == 32 && (policy.short_tiles || getenv("KRON_V12_SHORT"))) inst_sc = 42;
     int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     if (inst_s >= 0 && policy.short_tiles && dtype == KRON_F32 && p == 16) inst_s = 35;
-    const int inst_g = (p == q && allowed(3)) ? fused_find(dtype, p, 3) : -1;
+    // v4 chunk-pair GEMMs: not for fp64 P = 16, where the warp-chain kernel (v2) is faster (Table 3's fp64 16^6:
+    // 4.41 -> 3.89 ms, found by the autotuner, profiles/r02_sweeps/table3.jsonl); v4 stays an autotuner candidate
+    const int inst_g = (p == q && allowed(3) && !(dtype == KRON_F64 && p == 16 && policy.kinds == 0xFFFFu))
+                           ? fused_find(dtype, p, 3)
+                           : -1;
     const int inst_p = (p == q && allowed(2)) ? fused_find(dtype, p, 2) : -1;
     const int inst_w = (p == q && allowed(1)) ? fused_find(dtype, p, 1) : -1;
     const int inst_c = (p == q) ? fused_find(dtype, p, 0) : -1;  // always allowed: any chunk size
