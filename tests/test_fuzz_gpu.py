@@ -65,7 +65,7 @@ def _shapes(n=120, seed=2401):
     return out
 
 
-@pytest.mark.parametrize("M,P,Q,dt", _shapes() + _shapes(120, seed=10187))
+@pytest.mark.parametrize("M,P,Q,dt", _shapes() + _shapes(120, seed=10187) + _shapes(120, seed=2026))
 def test_fuzz_bit_exact(cuda_device, M, P, Q, dt):
     import torch
     from paper_2401_10187_b200 import kron
