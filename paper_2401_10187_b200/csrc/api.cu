@@ -336,7 +336,7 @@ kron_status_t make_plan(int64_t M, int N, const int32_t *P, const int32_t *Q, in
     const int inst_3 = (p == q && allowed(10)) ? fused_find(dtype, p, 10) : -1;
     const int inst_3c = (p == q && allowed(12)) ? fused_find(dtype, p, 12) : -1;  // v10 triple
     int inst_sc = (p == q && allowed(11)) ? fused_find(dtype, p, 11) : -1;  // v10 pair (P = 16) / v12 pair (P = 32)
-    if (inst_sc >= 0 && dtype == KRON_F32 && p == 32 && (policy.short_tiles || getenv("KRON_V12_SHORT"))) inst_sc = 42;
+    if (inst_sc >= 0 && dtype == KRON_F32 && p == 32 && policy.short_tiles) inst_sc = 42;  // autotuner candidate
     int inst_s = (p == q && allowed(6)) ? fused_find(dtype, p, 6) : -1;
     if (inst_s >= 0 && policy.short_tiles && dtype == KRON_F32 && p == 16) inst_s = 35;
     // v4 chunk-pair GEMMs: not for fp64 P = 16, where the warp-chain kernel (v2) is faster (Table 3's fp64 16^6:

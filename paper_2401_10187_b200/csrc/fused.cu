@@ -3114,16 +3114,16 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
       uint32_t box[3] = {(uint32_t)line, 256u, 1u};
       if (!encode_tmap(&tin, dtype, 3, in, dims, strides, box, true)) return (int)cudaErrorInvalidValue;
       smem = 1024 + (size_t)a.stages * 65536 + 24 * (size_t)a.stages;
-      // 16 compute warps (4 per SM sub-partition): E's triple 8.34 -> 8.13 ms vs 12 (8: 8.92)
-      static const int ncw = getenv("KRON_TRI_NCW") ? atoi(getenv("KRON_TRI_NCW")) : 16;  // A/B experiments only
-      threads = 32 * ((ncw == 16 ? 16 : ncw == 8 ? 8 : 12) + 4);
-      kt = ncw == 16 ? kron_tri_tm_kernel<16> : ncw == 8 ? kron_tri_tm_kernel<8> : kron_tri_tm_kernel<12>;
+      // 16 compute warps (4 per SM sub-partition): E's triple 8.13 ms vs 8.34 with 12 and 8.92 with 8
+      threads = 32 * (16 + 4);
+      kt = kron_tri_tm_kernel<16>;
     } else {
       // T''[row][g/4][u][g%4], u < WC (this pass's chunks), g < C = 256 (the producer's chunks): box {4, R, 64, 1}
       if (pp.nf != 2 || pp.C != 256 || pp.R != 64 || WC % pp.R) return (int)cudaErrorInvalidValue;
       if (a.push.on) {
         const int64_t upd = a.push.B / WC;  // composite columns per destination: a power of two >= 4
-        if (a.push.B % WC || (pp.Qc * WC) % a.push.B || upd < 4 || (upd & (upd - 1))) return (int)cudaErrorInvalidValue;
+        if (a.push.B % WC || (pp.Qc * WC) % a.push.B || upd < 4 || (upd & (upd - 1)) || pp.Qc / upd > kMaxPush)
+          return (int)cudaErrorInvalidValue;
       }
       a.tiles_k = (int)(WC / pp.R);
       a.ntiles = M * a.tiles_k;
