@@ -123,11 +123,14 @@ kron_status_t kron_graph_destroy(kron_graph_t *graph);
 
 /* Autotuning ("performs auto-tuning over a range of tile size parameter values for the
  * given shape ... find the kernel with the least execution time").  Candidate plans (fusion group
- * caps x kernel-family choices x fp64 DMMA on/off; duplicates removed) are each run once untimed and
- * `reps` times between CUDA events on `stream` with the caller's X, F and Y (Y receives the correct
- * result); the fastest is installed in the plan cache for (device, M, shapes, dtype), so subsequent
- * kron_matmul / kron_matmul_ws calls use it.  Synchronous (waits for `stream`).  *ncand receives the
- * number of distinct candidates and *best_ms the winner's mean time (both optional).              */
+ * caps x kernel-family choices x fp64 DMMA on/off x tile-major hand-off on/off x chain tile sizes;
+ * duplicates removed) are each run once untimed, then timed run by run between CUDA events on `stream`
+ * with the caller's X, F and Y (Y receives the correct result) in two sweeps over the candidates
+ * (forward, then reverse), `reps` runs each; a candidate's time is its fastest run, and it replaces the
+ * static plan only when more than 2% faster.  The winner is installed in the plan cache for (device,
+ * M, shapes, dtype), so subsequent kron_matmul / kron_matmul_ws calls use it.  Synchronous (waits for
+ * `stream`).  *ncand receives the number of distinct candidates and *best_ms the winner's time (both
+ * optional).                                                                                      */
 kron_status_t kron_autotune(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, const void *X,
                             const void *const *F, void *Y, kron_dtype_t dtype, int32_t reps, void *stream,
                             int32_t *ncand, float *best_ms);
