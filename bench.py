@@ -481,6 +481,12 @@ def measure_single(kron, synth, torch, cfg_name, args, dev, rank, barrier, mode=
         "gpu_launches": npass * args.steps, "clocks": clocks.summary(),
         "l2": "inputs larger than L2 (no flush)",
     }
+    # ALU-bound kernels under a power cap: the same achieved rate against the peak scaled to the measured SM clock
+    # (informational; `frac` stays against the max-clock peak)
+    clk = res["clocks"]
+    if roof.get("bound") == "alu" and clk.get("sm_mhz") and clk.get("sm_max_mhz"):
+        scale = float(clk["sm_mhz"]) / float(clk["sm_max_mhz"])
+        roof["frac_at_measured_clock"] = round(roof["frac"] / scale, 4) if scale > 0 else None
     return res, (X, Fs_h, Fs, Y, work, seed, dt, tdt, es, M, K, L, fl_step)
 
 
