@@ -2170,6 +2170,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
   } else {
     const int sw = warp - NCW;
     float *Y = reinterpret_cast<float *>(a.Y);
+    const int push_ush = a.push.on ? __ffs((int)(a.push.B / a.WC)) - 1 : 0;
     for (int it = 0;; ++it) {
       const int64_t tile = blockIdx.x + (int64_t)it * gridDim.x;
       if (tile >= a.ntiles) break;
@@ -2181,6 +2182,7 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
       if (rb < a.M) {
         const int64_t wc = a.WC;
         float *yr = Y + (int64_t)rb * a.Wout + (int64_t)cbk * R + lane;
+        const int64_t push_row = (int64_t)rb * a.push.B;
         // granule gk = 4*q2 + q1/4 holds composite columns u2 = 4*gk .. 4*gk+3 of every chunk
 #pragma unroll 1
         for (int gk = sw; gk < 64; gk += NSW) {
@@ -2190,13 +2192,12 @@ __global__ void __launch_bounds__((NCW + 4) * 32, 1) kron_pair_tm_kernel(const _
             if (a.push.on) {
               // distributed round: column c = u2*wc + chunk goes to destination d = c / B of the send block
               // send[d][row][B] (the pack fused into the store, as the v6 / v10 PUSH epilogues with rho = B, GK = 1);
-              // with B a multiple of wc (push.B = W / GK, wc = W / 256) d = u2 / (B / wc), no 64-bit division
-              // (B / wc = 256 / GK composite columns per destination, a power of two: shifts, no division)
+              // with B a multiple of wc (push.B = W / GK, wc = W / 256): d = u2 >> ush, B / wc = 2^ush composite
+              // columns per destination (ush computed once per warp, no division in the loop)
               const float vv[4] = {v.x, v.y, v.z, v.w};
-              const int ush = __ffs((int)(a.push.B / wc)) - 1;
-              const int d = (4 * gk) >> ush;  // the four columns 4gk .. 4gk+3 share a destination (B / wc >= 4)
-              float *sd = reinterpret_cast<float *>(a.push.dst[d]) + (int64_t)rb * a.push.B + (int64_t)cbk * R + h * 32 +
-                          lane + (int64_t)((4 * gk) & ((1 << ush) - 1)) * wc;
+              const int d = (4 * gk) >> push_ush;  // the four columns 4gk .. 4gk+3 share a destination (B / wc >= 4)
+              float *sd = reinterpret_cast<float *>(a.push.dst[d]) + push_row + (int64_t)cbk * R + h * 32 + lane +
+                          (int64_t)((4 * gk) & ((1 << push_ush) - 1)) * wc;
 #pragma unroll
               for (int j = 0; j < 4; ++j) sd[(int64_t)j * wc] = vv[j];
             } else {
