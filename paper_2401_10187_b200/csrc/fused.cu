@@ -1307,10 +1307,13 @@ __device__ __forceinline__ void cb_pair32(unsigned char *buf, uint32_t g0, int l
 // profiles/r01_microbench_scatter.jsonl) is why P = 16 uses 64-chunk (256-byte) tiles.
 // PUSH: distributed P2P round whose exchange is fused into this pass (NEXT-1): every output value is
 // stored at its StoreGPUTile position in the destination rank's heap instead of into Y (push_dst).
+// (32-bit index math: launch_fused refuses pushes with row widths >= 2^31 — a 64-bit division per value had made
+// the pushing epilogues several times slower than the plain stores)
 template <typename T>
 __device__ __forceinline__ T *push_dst(const FusedArgs &a, int rb, int64_t col) {
-  const int64_t d = col / a.push.B, e = col - d * a.push.B, run = e / a.push.rho;
-  const int64_t tcol = (run * a.push.GK + a.push.me) * a.push.rho + (e - run * a.push.rho);
+  const uint32_t c = (uint32_t)col, B = (uint32_t)a.push.B, rho = (uint32_t)a.push.rho;
+  const uint32_t d = c / B, e = c - d * B, run = e / rho;
+  const uint32_t tcol = (run * (uint32_t)a.push.GK + (uint32_t)a.push.me) * rho + (e - run * rho);
   return reinterpret_cast<T *>(a.push.dst[d]) + (int64_t)rb * a.push.wd + tcol;
 }
 
@@ -1883,10 +1886,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__((NCW + 4) * 32, 1)
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
               const int64_t col = (int64_t)(u0 + j) * wc + (int64_t)gj * 8 + h * 4;
-              const int64_t d = col / a.push.B, e = col - d * a.push.B;
-              const int64_t run = e / a.push.rho;
-              const int64_t tcol = (run * a.push.GK + a.push.me) * a.push.rho + (e - run * a.push.rho);
-              *reinterpret_cast<float4 *>(reinterpret_cast<T *>(a.push.dst[d]) + (int64_t)rb * a.push.wd + tcol) = o4[j];
+              *reinterpret_cast<float4 *>(push_dst<T>(a, rb, col)) = o4[j];
             }
           }
         }
@@ -3249,6 +3249,7 @@ int launch_fused(const PassPlan &pp, int dtype, int64_t M, const void *in, void 
   if (push && push->on) {
     if ((inst.warp != 10 && inst.warp != 6 && inst.warp != 11 && inst.warp != 12) || push->GK > kMaxPush)
       return (int)cudaErrorInvalidValue;
+    if (Wout >= (int64_t(1) << 31) || push->wd >= (int64_t(1) << 31)) return (int)cudaErrorInvalidValue;  // push_dst
     a.push = *push;
   }
   // v10: this launch's factors go to a constant-bank slot first (stream-ordered)
