@@ -260,31 +260,32 @@ __global__ void p2p_barrier_kernel(PeerPtrs heaps, unsigned long long *my_flags,
 }
 
 // Pull + StoreGPUTile.  V = elements per vector (16 bytes when rho*es and the offsets allow, else 1).
-template <typename T, int V>
+// I: the index type — 32-bit when rows * Wl / V < 2^31 (the divisions per vector are then 32-bit: a 64-bit
+// division is several times the cost)
+template <typename T, int V, typename I>
 __global__ void __launch_bounds__(256) p2p_pull_kernel(PeerPtrs outs, T *__restrict__ dst, int64_t rows, int64_t Wl,
                                                        int64_t rho, int GK, int me) {
   using Vec = typename std::conditional<V == 1, T, uint4>::type;
-  const int64_t B = Wl / GK, rv = rho / V, n = rows * (Wl / V);
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+  const I wv = (I)(Wl / V), B = (I)(Wl / GK), rv = (I)(rho / V), n = (I)(rows * (Wl / V)), gk = (I)GK;
+  const I stride = (I)gridDim.x * (I)blockDim.x;
+  for (I i0 = (I)blockIdx.x * (I)blockDim.x + (I)threadIdx.x; i0 < n; i0 += 4 * stride) {
     Vec v[4];
-    int64_t di[4];
+    bool ok[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {  // four independent remote loads in flight per thread
-      const int64_t i = i0 + u * stride;
-      di[u] = -1;
-      if (i < n) {
-        const int64_t m = i / (Wl / V), c = i - m * (Wl / V);
-        const int64_t run = c / rv, t = c - run * rv;
-        const int64_t e = run / GK, src = run - e * GK;
-        const Vec *s = reinterpret_cast<const Vec *>(outs.p[src]) + m * (Wl / V) + me * (B / V) + e * rv + t;
+      const I i = i0 + (I)u * stride;
+      ok[u] = i < n;
+      if (ok[u]) {
+        const I m = i / wv, c = i - m * wv;
+        const I run = c / rv, t = c - run * rv;
+        const I e = run / gk, src = run - e * gk;
+        const Vec *s = reinterpret_cast<const Vec *>(outs.p[src]) + (int64_t)m * wv + (int64_t)me * (B / V) + e * rv + t;
         v[u] = *s;
-        di[u] = i;
       }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      if (di[u] >= 0) reinterpret_cast<Vec *>(dst)[di[u]] = v[u];
+      if (ok[u]) reinterpret_cast<Vec *>(dst)[(int64_t)i0 + (int64_t)u * stride] = v[u];
   }
 }
 
@@ -299,12 +300,23 @@ int launch_p2p_pull(int dtype, const PeerPtrs &outs, void *dst, int64_t rows, in
   int64_t blocks = (n / (vec ? V : 1) + 1023) / 1024;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (blocks < 1) blocks = 1;
+  const bool small = n < (int64_t(1) << 31) - 4 * 148 * 8 * 256;  // 32-bit indices cannot overflow
   if (dtype == KRON_F32) {
-    if (vec) p2p_pull_kernel<float, 4><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
-    else p2p_pull_kernel<float, 1><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+    if (small) {
+      if (vec) p2p_pull_kernel<float, 4, uint32_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+      else p2p_pull_kernel<float, 1, uint32_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+    } else {
+      if (vec) p2p_pull_kernel<float, 4, int64_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+      else p2p_pull_kernel<float, 1, int64_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (float *)dst, rows, Wl, rho, GK, me);
+    }
   } else {
-    if (vec) p2p_pull_kernel<double, 2><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
-    else p2p_pull_kernel<double, 1><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+    if (small) {
+      if (vec) p2p_pull_kernel<double, 2, uint32_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+      else p2p_pull_kernel<double, 1, uint32_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+    } else {
+      if (vec) p2p_pull_kernel<double, 2, int64_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+      else p2p_pull_kernel<double, 1, int64_t><<<(unsigned)blocks, 256, 0, s>>>(outs, (double *)dst, rows, Wl, rho, GK, me);
+    }
   }
   return (int)cudaGetLastError();
 }
