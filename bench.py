@@ -642,6 +642,7 @@ def run_dist(args, kron, synth, torch, ws, rank, local, dev, barrier):
     alu_peak = FP32_PEAK_TFLOPS if es == 4 else FP64_PEAK_TFLOPS
     t_roof = max(b_alg / (hbm_peak * 1e9), f_alg / (alu_peak * 1e12)) / ws
     round_info = ctx.round_info(M, P, Q, tdt) if ctx.GK > 1 else []
+    round_layouts = ctx.round_layouts(M, P, Q, tdt) if ctx.GK > 1 and hasattr(ctx, "round_layouts") else []
 
     # e2e: this rank's block from pinned host memory -> kron_matmul_dist -> Y_local back to pinned host memory
     e2e = None
@@ -683,7 +684,8 @@ def run_dist(args, kron, synth, torch, ws, rank, local, dev, barrier):
             "data": "synthetic (seeded counter-based U[0,1), each rank generates its own block in HBM)",
             "config": {"workload": cfg_name, "M": M, "P": P, "Q": Q, "grid": [ctx.GM, ctx.GK],
                        "rounds": rounds, "exchanged_values_per_step": int(sum(ledger)),
-                       "fused_layout_per_round": round_info, "row_chunks": args.chunks,
+                       "fused_layout_per_round": round_info, "exchange_layout_per_round": round_layouts,
+                       "row_chunks": args.chunks,
                        "parallelism": f"Algorithm 2 grid {ctx.GM}x{ctx.GK} (rows x K), " +
                                       ("NCCL all-to-all" if ctx.backend == "nccl" else
                                        "P2P over peer memory (CUDA IPC)" if ctx.backend == "p2p" else

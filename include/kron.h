@@ -222,6 +222,12 @@ kron_status_t kron_dist_sync(kron_dist_ctx_t *ctx, void *stream, int32_t timeout
 kron_status_t kron_dist_round_info(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
                                    const kron_dist_ctx_t *ctx, int32_t cap, int32_t *nrounds, int32_t *fused_send,
                                    int32_t *fused_recv);
+/* Per round (host only, up to `cap`): the exchange layout backends 0 / 1 use — 0 plain block + pack /
+ * StoreGPUTile kernels, 1 fused direct-index send / receive layouts (above), 2 the v11 tile-major layouts
+ * (config E's rounds [16^3, 16^2]: the triple writes the send blocks tile-major, the pair reads the receive
+ * blocks through a 4-D map).  Same errors as kron_dist_round_info. */
+kron_status_t kron_dist_round_layouts(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                      const kron_dist_ctx_t *ctx, int32_t cap, int32_t *nrounds, int32_t *layout);
 /* Grid actually used by the context. */
 kron_status_t kron_dist_ctx_grid(const kron_dist_ctx_t *ctx, int32_t *GM, int32_t *GK);
 /* Fill a 128-byte buffer with a fresh ncclUniqueId (rank 0 calls this, then broadcasts it). */

@@ -442,6 +442,26 @@ struct RoundPlan {
   int tm = 0;           // backends 0/1, config-E rounds [16^3, 16^2]: v11 tile-major layouts (1 triple, 2 pair)
 };
 
+// v11 hand-off through the exchange (fused.cu kron_tri_tm_kernel): rounds [16^3 triple, 16^2 pair] on fp32 — the
+// triple writes the send blocks tile-major (each destination's u range), the pair reads the receive blocks through
+// a 4-D map whose box lands in the single-GPU tile layout, and pushes its outputs into the final send blocks; the
+// values and the exchanged volume are those of the direct-index rounds.  plans[j][v]: round j's local plans (full
+// and ragged row chunk); wl_in[j]: round j's local input width.
+bool tile_major_rounds(int dtype, int N, const int32_t *P, const int32_t *Q, int GK, const std::vector<int> &rounds,
+                       const Plan *const (*plans)[2], const int64_t *wl_in, bool fused, bool p2p) {
+  static const bool no_handoff = getenv("KRON_NO_HANDOFF") != nullptr;
+  bool tm = !p2p && fused && !no_handoff && dtype == KRON_F32 && rounds.size() == 2 && rounds[0] == 3 &&
+            rounds[1] == 2 && GK <= kMaxPush && 64 % GK == 0;
+  for (int i = 0; i < N && tm; ++i) tm &= P[i] == 16 && Q[i] == 16;
+  for (int j = 0; j < 2 && tm; ++j)
+    for (int v = 0; v < 2; ++v) {
+      const Plan &pl = *plans[j][v];
+      tm &= pl.passes.size() == 1 && pl.passes[0].kind == KIND_FUSED && !pl.passes[0].tc_mode &&
+            fused_instance(pl.passes[0].variant).warp == (j == 0 ? 12 : 11) && pl.passes[0].R == (j == 0 ? 8 : 64);
+    }
+  return tm && (wl_in[0] / 4096) % 4 == 0 && 4096 % (32 * GK) == 0 && (wl_in[1] / 256) % 64 == 0;
+}
+
 inline char *at(void *p, int64_t elems, size_t es) { return static_cast<char *>(p) + (size_t)elems * es; }
 inline const char *at(const void *p, int64_t elems, size_t es) { return static_cast<const char *>(p) + (size_t)elems * es; }
 
@@ -739,6 +759,45 @@ kron_status_t kron_dist_round_info(int64_t M, int32_t N, const int32_t *P, const
   return KRON_OK;
 }
 
+kron_status_t kron_dist_round_layouts(int64_t M, int32_t N, const int32_t *P, const int32_t *Q, kron_dtype_t dtype,
+                                      const kron_dist_ctx_t *ctx, int32_t cap, int32_t *nrounds, int32_t *layout) {
+  if (!ctx || !nrounds || (cap > 0 && !layout)) return KRON_ERR_INVALID_ARG;
+  std::vector<int32_t> fs(64), fr(64);
+  kron_status_t st = kron_dist_round_info(M, N, P, Q, dtype, ctx, 64, nrounds, fs.data(), fr.data());
+  if (st != KRON_OK) return st;
+  std::vector<int> rounds;
+  if ((st = dist_round_plan(M, N, P, Q, ctx->GM, ctx->GK, &rounds, nullptr)) != KRON_OK) return st;
+  bool tm = false;
+  if (rounds.size() == 2 && ctx->GK > 1) {
+    // the same check kron_matmul_dist makes, on the plans of the full and the ragged row chunk
+    const int GK = ctx->GK;
+    std::vector<int64_t> W(N + 1);
+    W[N] = 1;
+    for (int i = 0; i < N; ++i) W[N] *= P[i];
+    for (int f = N; f >= 1; --f) W[f - 1] = W[f] / P[f - 1] * Q[f - 1];
+    const int64_t Ml = M / ctx->GM, nc = std::max<int64_t>(1, std::min<int64_t>(ctx->nchunks, Ml));
+    const int64_t rows0 = (Ml + nc - 1) / nc, nchunk = (Ml + rows0 - 1) / rows0, rows_last = Ml - (nchunk - 1) * rows0;
+    Plan pl[2][2];
+    int64_t wl[2];
+    int f = N;
+    for (int j = 0; j < 2 && st == KRON_OK; ++j) {
+      const int k = rounds[j];
+      int64_t C = 1;
+      for (int i = 0; i < k; ++i) C *= P[f - 1 - i];
+      wl[j] = W[f] / GK;
+      for (int v = 0; v < 2 && st == KRON_OK; ++v)
+        st = make_plan(std::max<int64_t>(v == 0 ? rows0 : rows_last, 1), k, P + (f - k), Q + (f - k), (int)dtype,
+                       &pl[j][v], wl[j] / C);
+      f -= k;
+    }
+    if (st != KRON_OK) return st;
+    const Plan *const pls[2][2] = {{&pl[0][0], &pl[0][1]}, {&pl[1][0], &pl[1][1]}};
+    tm = tile_major_rounds((int)dtype, N, P, Q, GK, rounds, pls, wl, ctx->fused, ctx->backend == 2);
+  }
+  for (int j = 0; j < *nrounds && j < cap; ++j) layout[j] = tm ? 2 : (fs[j] || fr[j]) ? 1 : 0;
+  return KRON_OK;
+}
+
 }  // extern "C"
 
 namespace kron {
@@ -904,22 +963,11 @@ kron_status_t kron_matmul_dist(int64_t M, int32_t N, const int32_t *P, const int
       max_w = std::max(max_w, std::max(R.wl_in, R.wl_out));
       f -= R.k;
     }
-    // v11 hand-off through the exchange (fused.cu kron_tri_tm_kernel): rounds [16^3 triple, 16^2 pair] on fp32 —
-    // the triple writes the send blocks tile-major (each destination's u range), the pair reads the receive
-    // blocks through a 4-D map whose box lands in the single-GPU tile layout, and pushes its outputs into the
-    // final send blocks; the values and the exchanged volume are those of the direct-index rounds
-    static const bool no_handoff = getenv("KRON_NO_HANDOFF") != nullptr;
-    bool tm = !p2p && ctx->fused && !no_handoff && dtype == KRON_F32 && rounds.size() == 2 && rounds[0] == 3 &&
-              rounds[1] == 2 && GK <= kMaxPush && 64 % GK == 0;
-    for (int i = 0; i < N; ++i) tm &= P[i] == 16 && Q[i] == 16;
-    for (int j = 0; j < 2 && tm; ++j)
-      for (int v = 0; v < 2; ++v) {
-        const Plan &pl = rp[j].plan[v];
-        tm &= pl.passes.size() == 1 && pl.passes[0].kind == KIND_FUSED && !pl.passes[0].tc_mode &&
-              fused_instance(pl.passes[0].variant).warp == (j == 0 ? 12 : 11) && pl.passes[0].R == (j == 0 ? 8 : 64);
-      }
-    if (tm) {
-      tm &= (rp[0].wl_in / 4096) % 4 == 0 && 4096 % (32 * GK) == 0 && (rp[1].wl_in / 256) % 64 == 0;
+    bool tm = false;
+    if (rounds.size() == 2) {
+      const Plan *const pls[2][2] = {{&rp[0].plan[0], &rp[0].plan[1]}, {&rp[1].plan[0], &rp[1].plan[1]}};
+      const int64_t wl[2] = {rp[0].wl_in, rp[1].wl_in};
+      tm = tile_major_rounds((int)dtype, N, P, Q, GK, rounds, pls, wl, ctx->fused, p2p);
     }
     if (tm) {
       rp[0].tm = 1;

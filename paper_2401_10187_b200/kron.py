@@ -350,6 +350,9 @@ _lib.kron_dist_ctx_set.restype = ctypes.c_int
 _lib.kron_dist_ctx_set.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32]
 _lib.kron_dist_sync.restype = ctypes.c_int
 _lib.kron_dist_sync.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32]
+_lib.kron_dist_round_layouts.restype = ctypes.c_int
+_lib.kron_dist_round_layouts.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, ctypes.c_void_p,
+                                         ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
 _lib.kron_dist_round_info.restype = ctypes.c_int
 _lib.kron_dist_round_info.argtypes = [ctypes.c_int64, ctypes.c_int32, _i32p, _i32p, ctypes.c_int, ctypes.c_void_p,
                                       ctypes.c_int32, _i32p, _i32p, _i32p]
@@ -422,6 +425,15 @@ class DistContext:
         _check(_lib.kron_dist_round_info(M, len(P), Pa, Qa, dtype_code(dtype), self.handle, 64, ctypes.byref(n),
                                          fs, fr), "kron_dist_round_info")
         return [(bool(fs[i]), bool(fr[i])) for i in range(n.value)]
+
+    def round_layouts(self, M, P, Q, dtype):
+        """Per round: the exchange layout of backends 0 / 1 — "plain", "direct-index" or "tile-major" (host only)."""
+        Pa, Qa = _shape_arrays(P, Q)
+        n = ctypes.c_int32()
+        lay = (ctypes.c_int32 * 64)()
+        _check(_lib.kron_dist_round_layouts(M, len(P), Pa, Qa, dtype_code(dtype), self.handle, 64, ctypes.byref(n), lay),
+               "kron_dist_round_layouts")
+        return [("plain", "direct-index", "tile-major")[lay[i]] for i in range(n.value)]
 
     def ensure_heap(self, nbytes: int) -> None:
         """P2P backend: (re)reserve the symmetric heap if it is smaller than `nbytes` and map the peers'

@@ -247,7 +247,15 @@ def test_dist_round_info_fused_layouts(kron):
     assert ctx3.round_info(1024, [32] * 4, [32] * 4, "float32") == [(False, False), (False, False)]
     with pytest.raises(kron.KronError):
         kron.DistContext("virtual", GM=1, GK=2, chunks=0)
-    for c in (ctx, ctx2, ctx3):
+    # exchange layouts: config E's rounds on the v11 tile-major layouts (fp32 only, fused layouts on), the rest
+    # direct-index or plain
+    assert ctx.round_layouts(4096, [16] * 5, [16] * 5, "float32") == ["tile-major", "tile-major"]
+    assert ctx.round_layouts(4096, [16] * 5, [16] * 5, "float64") != ["tile-major", "tile-major"]
+    assert ctx2.round_layouts(1024, [32] * 4, [32] * 4, "float32") == ["direct-index", "direct-index"]
+    assert ctx3.round_layouts(4096, [16] * 5, [16] * 5, "float32") == ["plain", "plain"]
+    ctx8 = kron.DistContext("virtual", GM=1, GK=8)
+    assert ctx8.round_layouts(64, [16] * 5, [16] * 5, "float32") == ["tile-major", "tile-major"]
+    for c in (ctx, ctx2, ctx3, ctx8):
         c.close()
 
 
